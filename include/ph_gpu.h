@@ -1,0 +1,112 @@
+/* ph_gpu.h — C ABI of the B200 (sm_100a) PtrHash query path.
+ *
+ * Drop-in boundary for the reference's query API, PtrHashIndex
+ * (/root/reference/proj/include/ptrhash/index.hpp:58-81). The index is the
+ * reference's own serialized PTRH v1 file (proj/include/ptrhash/serde.hpp:12-31),
+ * uploaded unchanged to one GPU; every query returns exactly the reference's value.
+ *
+ * Conventions:
+ *  - integer status, PH_OK == 0; no exceptions cross the ABI; message via
+ *    ph_gpu_last_error() (thread-local);
+ *  - a ph_gpu_index is immutable after create and safe to use from any number of
+ *    host threads and CUDA streams at once (index.hpp:26-31);
+ *  - device-pointer entry points are asynchronous on the given stream
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream);
+ *  - host-pointer entry points are synchronous, like the reference's methods;
+ *  - queries have no error path for non-member keys: they return an arbitrary
+ *    value below n (minimal) or below P*S (non-minimal), as index.hpp:26-31.
+ */
+#ifndef PH_GPU_H
+#define PH_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ph_gpu_index ph_gpu_index; /* opaque, immutable after create */
+typedef void* ph_gpu_stream_t;            /* cudaStream_t */
+
+enum ph_gpu_status {
+    PH_OK = 0,
+    PH_E_INVALID = 1,  /* bad argument (null pointer, bad width, ...) */
+    PH_E_FORMAT = 2,   /* malformed PTRH bytes; same checks as serde.cpp:176-240 */
+    PH_E_CUDA = 3,     /* CUDA runtime error (no device, launch failure, ...) */
+    PH_E_KEYKIND = 4,  /* u64 query on a string index or vice versa (index.hpp:18-21) */
+    PH_E_NOMEM = 5,    /* device or pinned-host allocation failed */
+    PH_E_UNSUPPORTED = 6 /* shape outside what the GPU path supports */
+};
+
+/* Output element width for bulk queries: u32 (all configs, n <= 2^32) or u64
+ * (the reference's `uint64_t* out`, index.hpp:72-81). */
+enum { PH_OUT_U32 = 4, PH_OUT_U64 = 8 };
+
+typedef struct ph_gpu_info {
+    uint64_t n;                /* keys (Shape::n, shape.hpp:65-75) */
+    uint64_t parts;            /* P */
+    uint64_t slots_per_part;   /* S */
+    uint64_t buckets_per_part; /* B */
+    uint64_t seed;
+    uint64_t pilot_bytes;      /* P*B */
+    uint64_t remap_values;     /* P*S - n */
+    uint64_t remap_bytes;      /* payload bytes resident on the device */
+    uint8_t key_kind;          /* 0 u64, 1 bytes (index.hpp:18-21) */
+    uint8_t hash_algo;         /* hash.hpp:37-43 */
+    uint8_t bucket_fn;         /* shape.hpp:23-29 */
+    uint8_t remap_kind;        /* shape.hpp:31-35 */
+    uint8_t reduce_kind;       /* header id (reduce.hpp:11-20); informational */
+    uint8_t pow2;              /* reduce path actually used: is_power_of_two(S), reduce.hpp:51 */
+    int32_t device;
+} ph_gpu_info;
+
+/* Parse + validate PTRH v1 bytes (serde.cpp:176-240) and upload pilots and the
+ * remap payload to `device`. Replaces deserialize()/load_index() + the
+ * PtrHashIndex ctor (serde.cpp:176-260, index.hpp:36-46). */
+int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_index** out);
+int ph_gpu_index_destroy(ph_gpu_index* index);
+int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out);
+const char* ph_gpu_last_error(void);
+
+/* ---- device-resident bulk queries (asynchronous on `stream`) ----
+ * Replace PtrHashIndex::index_loop / index_batched / index_stream
+ * (index.hpp:72-81, index.cpp:15-137): out[i] = minimal ? index(keys[i])
+ * : index_no_remap(keys[i]). d_out holds n elements of `out_width` bytes. */
+int ph_gpu_query_u64(const ph_gpu_index* index, const uint64_t* d_keys, size_t n, void* d_out,
+                     int out_width, int minimal, ph_gpu_stream_t stream);
+
+/* String keys as one concatenated byte buffer + offsets[n+1] (key i is
+ * bytes[offsets[i] .. offsets[i+1])). Replaces the span<const std::string>
+ * overloads (index.hpp:77-81) with hash_bytes (hash.cpp:159-193). */
+int ph_gpu_query_bytes(const ph_gpu_index* index, const uint8_t* d_bytes,
+                       const uint64_t* d_offsets, size_t n, void* d_out, int out_width,
+                       int minimal, ph_gpu_stream_t stream);
+
+/* ---- host-resident bulk queries (synchronous; the reference's own signature
+ * shape: host keys in, host `out` fully overwritten) ----
+ * Pipelined H2D -> kernel -> D2H over chunks on several streams. Pinned host
+ * buffers are used directly; pageable ones are staged through pinned bounce
+ * buffers. */
+int ph_gpu_index_stream_u64(const ph_gpu_index* index, const uint64_t* h_keys, size_t n,
+                            void* h_out, int out_width, int minimal);
+int ph_gpu_index_stream_bytes(const ph_gpu_index* index, const uint8_t* h_bytes,
+                              const uint64_t* h_offsets, size_t n, void* h_out, int out_width,
+                              int minimal);
+
+/* ---- single-key queries (synchronous): index() / index_no_remap(),
+ * index.hpp:60-64 ---- */
+int ph_gpu_index_u64(const ph_gpu_index* index, uint64_t key, int minimal, uint64_t* out);
+int ph_gpu_index_bytes(const ph_gpu_index* index, const uint8_t* key, size_t len, int minimal,
+                       uint64_t* out);
+
+/* ---- introspection ---- */
+/* Number of query-kernel launches this process made through this library. */
+uint64_t ph_gpu_launch_count(void);
+/* Override the bulk-kernel launch shape (0 = automatic). For tuning/bench. */
+int ph_gpu_set_launch(int threads_per_block, int blocks_per_sm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PH_GPU_H */

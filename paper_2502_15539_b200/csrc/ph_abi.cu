@@ -1,0 +1,606 @@
+// ph_abi.cu — host side of the C ABI (include/ph_gpu.h).
+//
+//  * PTRH v1 parsing and validation, mirroring deserialize()
+//    (/root/reference/proj/src/serde.cpp:176-240) check for check;
+//  * device upload: pilots and CacheLineEF/plain32 payload byte-identical to
+//    the file; Elias-Fano's three u64 arrays re-aligned (serde.cpp:93-101);
+//    the optimal-gamma table computed on the host exactly as
+//    bucket_fn.cpp:16-39 does (double ln, monotone clamp) and uploaded;
+//  * the query entry points: device-resident (async) and host-resident
+//    (pipelined H2D -> kernel -> D2H over chunks and streams, synchronous).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ph_gpu.h"
+#include "ph_device.cuh"
+#include "ph_kernels.h"
+
+using u128 = unsigned __int128;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(PH_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PH_CUDA(call)                                 \
+    do {                                              \
+        cudaError_t e_ = (call);                      \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+uint64_t le64(const uint8_t* p) {
+    uint64_t v;
+    std::memcpy(&v, p, 8);
+    return v;
+}
+uint32_t le32(const uint8_t* p) {
+    uint32_t v;
+    std::memcpy(&v, p, 4);
+    return v;
+}
+bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+// Sets the device for the scope of one ABI call and restores the caller's.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// bucket_fn.cpp:16-39 — filled with double-precision ln, monotonized.
+void optimal_table(std::vector<uint64_t>& t) {
+    t.resize(65537);
+    const double eps = 1.0 / 256.0;
+    const double scale = std::ldexp(1.0, 64);
+    uint64_t prev = 0;
+    for (size_t i = 0; i <= 65536; i++) {
+        const double x = static_cast<double>(i) / 65536;
+        double y = x;
+        if (x < 1.0) y = x + (1.0 - eps) * (1.0 - x) * std::log(1.0 - x);
+        const double scaled = y * scale;
+        uint64_t u;
+        if (scaled >= scale) u = UINT64_MAX;
+        else if (scaled <= 0.0) u = 0;
+        else u = static_cast<uint64_t>(scaled);
+        if (u < prev) u = prev;
+        t[i] = u;
+        prev = u;
+    }
+}
+
+}  // namespace
+
+struct ph_gpu_index {
+    int device = 0;
+    int sms = 148;
+    ph_gpu_info info{};
+    phg::DevIndex dev{};
+    void* d_pilots = nullptr;
+    void* d_remap = nullptr;
+    void* d_ef[3] = {nullptr, nullptr, nullptr};
+    void* d_opt = nullptr;
+};
+
+namespace {
+
+// PTRH v1 (serde.hpp:12-31) -> validated header + payload views.
+struct Parsed {
+    uint8_t key_kind, algo, bucket_fn, remap_kind, reduce_kind;
+    uint64_t n, P, S, B, seed, pilots_len, remap_len;
+    const uint8_t* pilots;
+    const uint8_t* remap;
+    // Elias-Fano
+    uint64_t ef_count = 0, ef_universe = 0;
+    uint8_t ef_low_bits = 0;
+    std::vector<uint64_t> ef[3];
+};
+
+int parse_ptrh(const uint8_t* b, size_t len, Parsed& p) {
+    if (!b) return fail(PH_E_INVALID, "null index bytes");
+    if (len < 4) return fail(PH_E_FORMAT, "index file truncated");
+    if (std::memcmp(b, "PTRH", 4) != 0) return fail(PH_E_FORMAT, "not an index file (bad magic)");
+    if (len < 72) return fail(PH_E_FORMAT, "index file truncated");
+    const uint32_t version = le32(b + 4);
+    if (version != 1)
+        return fail(PH_E_FORMAT, "unsupported index format version " + std::to_string(version));
+    p.key_kind = b[8];
+    p.algo = b[9];
+    p.bucket_fn = b[10];
+    p.remap_kind = b[11];
+    p.reduce_kind = b[12];
+    if (p.key_kind > 1) return fail(PH_E_FORMAT, "unknown key kind id");
+    if (p.algo > 4) return fail(PH_E_FORMAT, "unknown hash algorithm id");
+    if (p.bucket_fn > 4) return fail(PH_E_FORMAT, "unknown bucket function id");
+    if (p.remap_kind > 2) return fail(PH_E_FORMAT, "unknown remap kind id");
+    if (p.reduce_kind > 2) return fail(PH_E_FORMAT, "unknown reduce kind id");
+    // No AES-NI requirement (serde.cpp:200-202): the GPU computes AES itself.
+    p.n = le64(b + 16);
+    p.P = le64(b + 24);
+    p.S = le64(b + 32);
+    p.B = le64(b + 40);
+    p.seed = le64(b + 48);
+    p.pilots_len = le64(b + 56);
+    p.remap_len = le64(b + 64);
+    if (p.n == 0 || p.P == 0 || p.S == 0) return fail(PH_E_FORMAT, "index file: degenerate shape");
+    if ((u128)p.P * p.S > ((u128)1 << 62) || (u128)p.P * p.B > ((u128)1 << 62))
+        return fail(PH_E_FORMAT, "index file: shape out of range");
+    if (p.n > p.P * p.S) return fail(PH_E_FORMAT, "index file: n exceeds the slot count");
+    if (p.pilots_len != p.P * p.B)
+        return fail(PH_E_FORMAT, "index file: pilot length does not match shape");
+    if ((u128)(len - 72) != (u128)p.pilots_len + p.remap_len)
+        return fail(PH_E_FORMAT, "index file: payload length mismatch");
+    p.pilots = b + 72;
+    p.remap = b + 72 + p.pilots_len;
+    const uint64_t count = p.P * p.S - p.n;
+    switch (p.remap_kind) {
+        case 0:
+            if (p.remap_len != count * 4) return fail(PH_E_FORMAT, "index file: bad plain remap length");
+            break;
+        case 1:
+            if (p.remap_len != (count + 43) / 44 * 64)
+                return fail(PH_E_FORMAT, "index file: bad cacheline-ef remap length");
+            break;
+        case 2: {  // serde.cpp:119-136
+            size_t pos = 0;
+            auto need = [&](size_t k) { return pos + k <= p.remap_len; };
+            if (!need(17)) return fail(PH_E_FORMAT, "index file truncated");
+            p.ef_count = le64(p.remap);
+            p.ef_universe = le64(p.remap + 8);
+            p.ef_low_bits = p.remap[16];
+            pos = 17;
+            if (p.ef_count != count) return fail(PH_E_FORMAT, "index file: bad elias-fano count");
+            for (int a = 0; a < 3; a++) {
+                if (!need(8)) return fail(PH_E_FORMAT, "index file truncated");
+                const uint64_t m = le64(p.remap + pos);
+                pos += 8;
+                if (m > p.remap_len / 8 + 1)
+                    return fail(PH_E_FORMAT, "index file: array length out of range");
+                if (!need(m * 8)) return fail(PH_E_FORMAT, "index file truncated");
+                p.ef[a].resize(m);
+                for (uint64_t i = 0; i < m; i++) p.ef[a][i] = le64(p.remap + pos + 8 * i);
+                pos += m * 8;
+            }
+            if (pos != p.remap_len) return fail(PH_E_FORMAT, "index file: trailing bytes");
+            if (count > 0 && (p.ef[2].empty() || p.ef[1].empty()))
+                return fail(PH_E_FORMAT, "index file: bad elias-fano payload");
+            break;
+        }
+    }
+    if (!is_pow2(p.S) && p.S >= (uint64_t{1} << 32))
+        return fail(PH_E_FORMAT, "reduce: fastmod needs S < 2^32");  // reduce.hpp:56-57
+    return PH_OK;
+}
+
+int upload(const void* src, size_t bytes, void** dst) {
+    *dst = nullptr;
+    if (bytes == 0) return PH_OK;
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) return fail(PH_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(upload)");
+    return PH_OK;
+}
+
+void release(ph_gpu_index* ix) {
+    if (!ix) return;
+    DeviceGuard g(ix->device);
+    cudaFree(ix->d_pilots);
+    cudaFree(ix->d_remap);
+    for (void* p : ix->d_ef) cudaFree(p);
+    cudaFree(ix->d_opt);
+    delete ix;
+}
+
+int check_width(int w) {
+    return (w == PH_OUT_U32 || w == PH_OUT_U64) ? PH_OK
+                                                 : fail(PH_E_INVALID, "out_width must be 4 or 8");
+}
+
+int check_u32_range(const ph_gpu_index* ix, int out_width, int minimal) {
+    if (out_width == PH_OUT_U64) return PH_OK;
+    const uint64_t hi = minimal ? ix->info.n : ix->info.parts * ix->info.slots_per_part;
+    if (hi > (uint64_t{1} << 32))
+        return fail(PH_E_INVALID, "u32 output cannot hold indices up to " + std::to_string(hi));
+    return PH_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+bool is_pinned_host(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ph_gpu_last_error(void) { return g_err.c_str(); }
+uint64_t ph_gpu_launch_count(void) { return phg::launch_count(); }
+int ph_gpu_set_launch(int threads, int bps) {
+    if (threads != 0 && (threads < 32 || threads > 1024 || threads % 32))
+        return fail(PH_E_INVALID, "threads_per_block must be a multiple of 32 in [32,1024]");
+    phg::set_launch(threads, bps);
+    return PH_OK;
+}
+
+int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_index** out) {
+    if (!out) return fail(PH_E_INVALID, "null out handle");
+    *out = nullptr;
+    Parsed p;
+    if (int rc = parse_ptrh(ptrh, len, p)) return rc;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(PH_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(PH_E_INVALID, "bad device ordinal");
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+
+    auto* ix = new ph_gpu_index();
+    ix->device = device;
+    cudaDeviceGetAttribute(&ix->sms, cudaDevAttrMultiProcessorCount, device);
+    ph_gpu_info& I = ix->info;
+    I.n = p.n;
+    I.parts = p.P;
+    I.slots_per_part = p.S;
+    I.buckets_per_part = p.B;
+    I.seed = p.seed;
+    I.pilot_bytes = p.pilots_len;
+    I.remap_values = p.P * p.S - p.n;
+    I.key_kind = p.key_kind;
+    I.hash_algo = p.algo;
+    I.bucket_fn = p.bucket_fn;
+    I.remap_kind = p.remap_kind;
+    I.reduce_kind = p.reduce_kind;
+    I.pow2 = is_pow2(p.S) ? 1 : 0;
+    I.device = device;
+
+    int rc = upload(p.pilots, p.pilots_len, &ix->d_pilots);
+    if (!rc && p.remap_kind != 2) {
+        rc = upload(p.remap, p.remap_len, &ix->d_remap);
+        I.remap_bytes = p.remap_len;
+    }
+    if (!rc && p.remap_kind == 2) {
+        for (int a = 0; a < 3 && !rc; a++) {
+            rc = upload(p.ef[a].data(), p.ef[a].size() * 8, &ix->d_ef[a]);
+            I.remap_bytes += p.ef[a].size() * 8;
+        }
+    }
+    if (!rc && p.bucket_fn == 4) {
+        std::vector<uint64_t> t;
+        optimal_table(t);
+        rc = upload(t.data(), t.size() * 8, &ix->d_opt);
+    }
+    if (rc) {
+        release(ix);
+        return rc;
+    }
+    phg::DevIndex& d = ix->dev;
+    d.pilots = static_cast<const uint8_t*>(ix->d_pilots);
+    d.remap = static_cast<const uint8_t*>(ix->d_remap);
+    d.ef_low = static_cast<const uint64_t*>(ix->d_ef[0]);
+    d.ef_high = static_cast<const uint64_t*>(ix->d_ef[1]);
+    d.ef_samples = static_cast<const uint64_t*>(ix->d_ef[2]);
+    d.opt_table = static_cast<const uint64_t*>(ix->d_opt);
+    d.n = p.n;
+    d.P = p.P;
+    d.S = p.S;
+    d.B = p.B;
+    d.seed = p.seed;
+    if (!I.pow2) {  // FastModU64::make, reduce.hpp:31-36
+        const u128 m = ~u128{0} / p.S + 1;
+        d.magic_hi = static_cast<uint64_t>(m >> 64);
+        d.magic_lo = static_cast<uint64_t>(m);
+    }
+    d.hp_base = phg::kC * (p.seed & ~uint64_t{0xff});
+    d.seed_lo8 = static_cast<uint32_t>(p.seed & 0xff);
+    d.remap_kind = p.remap_kind;
+    d.ef_low_bits = p.ef_low_bits;
+    d.hash_algo = p.algo;
+    *out = ix;
+    return PH_OK;
+}
+
+int ph_gpu_index_destroy(ph_gpu_index* index) {
+    release(index);
+    return PH_OK;
+}
+
+int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out) {
+    if (!index || !out) return fail(PH_E_INVALID, "null argument");
+    *out = index->info;
+    return PH_OK;
+}
+
+int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, void* d_out,
+                     int out_width, int minimal, ph_gpu_stream_t stream) {
+    if (!ix) return fail(PH_E_INVALID, "null index");
+    if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
+    if (int rc = check_width(out_width)) return rc;
+    if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
+    if (n == 0) return PH_OK;
+    if (!d_keys || !d_out) return fail(PH_E_INVALID, "null key or output pointer");
+    DeviceGuard g(ix->device);
+    cudaError_t e = phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_keys, d_out,
+                                          out_width, n, minimal, static_cast<cudaStream_t>(stream),
+                                          ix->sms);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "query_u64 launch");
+}
+
+int ph_gpu_query_bytes(const ph_gpu_index* ix, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                       size_t n, void* d_out, int out_width, int minimal,
+                       ph_gpu_stream_t stream) {
+    if (!ix) return fail(PH_E_INVALID, "null index");
+    if (ix->info.key_kind != 1) return fail(PH_E_KEYKIND, "string query on a u64-key index");
+    if (int rc = check_width(out_width)) return rc;
+    if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
+    if (n == 0) return PH_OK;
+    if (!d_bytes || !d_offsets || !d_out) return fail(PH_E_INVALID, "null pointer argument");
+    DeviceGuard g(ix->device);
+    cudaError_t e = phg::launch_query_bytes(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_bytes,
+                                            d_offsets, 0, d_out, out_width, n, minimal,
+                                            static_cast<cudaStream_t>(stream), ix->sms);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "query_bytes launch");
+}
+
+// ---------------------------------------------------------------------------
+// host-resident bulk queries: chunked pipeline over kSlots streams
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kSlots = 3;
+
+struct Slot {
+    cudaStream_t s = nullptr;
+    void* d_in = nullptr;   // keys (u64) or bytes
+    void* d_off = nullptr;  // offsets (bytes path)
+    void* d_out = nullptr;
+    void* h_in = nullptr;   // pinned bounce buffers (pageable callers only)
+    void* h_off = nullptr;
+    void* h_out = nullptr;
+    size_t pend_off = 0, pend_n = 0;  // chunk whose output still sits in h_out
+    bool pending = false;
+};
+
+struct Pipeline {
+    Slot slot[kSlots];
+    ~Pipeline() {
+        for (Slot& s : slot) {
+            if (s.s) cudaStreamSynchronize(s.s);
+            cudaFree(s.d_in);
+            cudaFree(s.d_off);
+            cudaFree(s.d_out);
+            cudaFreeHost(s.h_in);
+            cudaFreeHost(s.h_off);
+            cudaFreeHost(s.h_out);
+            if (s.s) cudaStreamDestroy(s.s);
+        }
+    }
+};
+
+int alloc_pipeline(Pipeline& pl, size_t in_bytes, size_t off_bytes, size_t out_bytes,
+                   bool bounce) {
+    for (Slot& s : pl.slot) {
+        PH_CUDA(cudaStreamCreateWithFlags(&s.s, cudaStreamNonBlocking));
+        if (cudaMalloc(&s.d_in, in_bytes ? in_bytes : 1) != cudaSuccess ||
+            (off_bytes && cudaMalloc(&s.d_off, off_bytes) != cudaSuccess) ||
+            cudaMalloc(&s.d_out, out_bytes) != cudaSuccess)
+            return fail(PH_E_NOMEM, "device staging allocation failed");
+        if (bounce) {
+            if (cudaHostAlloc(&s.h_in, in_bytes ? in_bytes : 1, 0) != cudaSuccess ||
+                (off_bytes && cudaHostAlloc(&s.h_off, off_bytes, 0) != cudaSuccess) ||
+                cudaHostAlloc(&s.h_out, out_bytes, 0) != cudaSuccess)
+                return fail(PH_E_NOMEM, "pinned staging allocation failed");
+        }
+    }
+    return PH_OK;
+}
+
+size_t chunk_keys(size_t n) {
+    const size_t c = size_t{1} << 23;  // 8 Mi keys = 64 MiB of u64 keys per chunk
+    return n < c ? n : c;
+}
+
+}  // namespace
+
+int ph_gpu_index_stream_u64(const ph_gpu_index* ix, const uint64_t* h_keys, size_t n, void* h_out,
+                            int out_width, int minimal) {
+    if (!ix) return fail(PH_E_INVALID, "null index");
+    if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
+    if (int rc = check_width(out_width)) return rc;
+    if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
+    if (n == 0) return PH_OK;
+    if (!h_keys || !h_out) return fail(PH_E_INVALID, "null key or output pointer");
+    DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    if (is_device_ptr(h_keys) || is_device_ptr(h_out)) {  // device spans: no staging
+        if (int rc = ph_gpu_query_u64(ix, h_keys, n, h_out, out_width, minimal, nullptr)) return rc;
+        PH_CUDA(cudaStreamSynchronize(nullptr));
+        return PH_OK;
+    }
+    const size_t C = chunk_keys(n);
+    const bool bounce = !(is_pinned_host(h_keys) && is_pinned_host(h_out));
+    Pipeline pl;
+    if (int rc = alloc_pipeline(pl, C * 8, 0, C * out_width, bounce)) return rc;
+    auto* out_b = static_cast<uint8_t*>(h_out);
+    auto drain = [&](Slot& s) -> int {
+        if (!s.pending) return PH_OK;
+        PH_CUDA(cudaStreamSynchronize(s.s));
+        std::memcpy(out_b + s.pend_off * out_width, s.h_out, s.pend_n * out_width);
+        s.pending = false;
+        return PH_OK;
+    };
+    size_t c = 0;
+    for (size_t off = 0; off < n; off += C, c++) {
+        Slot& s = pl.slot[c % kSlots];
+        const size_t m = n - off < C ? n - off : C;
+        const void* src = h_keys + off;
+        void* dst = out_b + off * out_width;
+        if (bounce) {
+            if (int rc = drain(s)) return rc;
+            std::memcpy(s.h_in, h_keys + off, m * 8);
+            src = s.h_in;
+            dst = s.h_out;
+        }
+        PH_CUDA(cudaMemcpyAsync(s.d_in, src, m * 8, cudaMemcpyHostToDevice, s.s));
+        PH_CUDA(phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                      static_cast<const uint64_t*>(s.d_in), s.d_out, out_width, m,
+                                      minimal, s.s, ix->sms));
+        PH_CUDA(cudaMemcpyAsync(dst, s.d_out, m * out_width, cudaMemcpyDeviceToHost, s.s));
+        if (bounce) {
+            s.pending = true;
+            s.pend_off = off;
+            s.pend_n = m;
+        }
+    }
+    for (Slot& s : pl.slot) {
+        if (bounce) {
+            if (int rc = drain(s)) return rc;
+        } else {
+            PH_CUDA(cudaStreamSynchronize(s.s));
+        }
+    }
+    return PH_OK;
+}
+
+int ph_gpu_index_stream_bytes(const ph_gpu_index* ix, const uint8_t* h_bytes,
+                              const uint64_t* h_offsets, size_t n, void* h_out, int out_width,
+                              int minimal) {
+    if (!ix) return fail(PH_E_INVALID, "null index");
+    if (ix->info.key_kind != 1) return fail(PH_E_KEYKIND, "string query on a u64-key index");
+    if (int rc = check_width(out_width)) return rc;
+    if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
+    if (n == 0) return PH_OK;
+    if (!h_bytes || !h_offsets || !h_out) return fail(PH_E_INVALID, "null pointer argument");
+    DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    const size_t C = chunk_keys(n);
+    size_t max_bytes = 0;
+    for (size_t off = 0; off < n; off += C) {
+        const size_t m = n - off < C ? n - off : C;
+        const size_t b = h_offsets[off + m] - h_offsets[off];
+        if (b > max_bytes) max_bytes = b;
+    }
+    const bool bounce = !(is_pinned_host(h_bytes) && is_pinned_host(h_offsets) &&
+                          is_pinned_host(h_out));
+    Pipeline pl;
+    if (int rc = alloc_pipeline(pl, max_bytes, (C + 1) * 8, C * out_width, bounce)) return rc;
+    auto* out_b = static_cast<uint8_t*>(h_out);
+    auto drain = [&](Slot& s) -> int {
+        if (!s.pending) return PH_OK;
+        PH_CUDA(cudaStreamSynchronize(s.s));
+        std::memcpy(out_b + s.pend_off * out_width, s.h_out, s.pend_n * out_width);
+        s.pending = false;
+        return PH_OK;
+    };
+    size_t c = 0;
+    for (size_t off = 0; off < n; off += C, c++) {
+        Slot& s = pl.slot[c % kSlots];
+        const size_t m = n - off < C ? n - off : C;
+        const uint64_t b0 = h_offsets[off], b1 = h_offsets[off + m];
+        const void* src_b = h_bytes + b0;
+        const void* src_o = h_offsets + off;
+        void* dst = out_b + off * out_width;
+        if (bounce) {
+            if (int rc = drain(s)) return rc;
+            std::memcpy(s.h_in, h_bytes + b0, b1 - b0);
+            std::memcpy(s.h_off, h_offsets + off, (m + 1) * 8);
+            src_b = s.h_in;
+            src_o = s.h_off;
+            dst = s.h_out;
+        }
+        if (b1 > b0) PH_CUDA(cudaMemcpyAsync(s.d_in, src_b, b1 - b0, cudaMemcpyHostToDevice, s.s));
+        PH_CUDA(cudaMemcpyAsync(s.d_off, src_o, (m + 1) * 8, cudaMemcpyHostToDevice, s.s));
+        PH_CUDA(phg::launch_query_bytes(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                        static_cast<const uint8_t*>(s.d_in),
+                                        static_cast<const uint64_t*>(s.d_off), b0, s.d_out,
+                                        out_width, m, minimal, s.s, ix->sms));
+        PH_CUDA(cudaMemcpyAsync(dst, s.d_out, m * out_width, cudaMemcpyDeviceToHost, s.s));
+        if (bounce) {
+            s.pending = true;
+            s.pend_off = off;
+            s.pend_n = m;
+        }
+    }
+    for (Slot& s : pl.slot) {
+        if (bounce) {
+            if (int rc = drain(s)) return rc;
+        } else {
+            PH_CUDA(cudaStreamSynchronize(s.s));
+        }
+    }
+    return PH_OK;
+}
+
+// Single-key queries: one small device scratch block, synchronous.
+int ph_gpu_index_u64(const ph_gpu_index* ix, uint64_t key, int minimal, uint64_t* out) {
+    if (!ix || !out) return fail(PH_E_INVALID, "null argument");
+    if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
+    DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    uint64_t* d = nullptr;
+    PH_CUDA(cudaMalloc(&d, 16));
+    cudaError_t e = cudaMemcpy(d, &key, 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2, d, d + 1, 8, 1,
+                                  minimal, nullptr, ix->sms);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d + 1, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "index_u64");
+}
+
+int ph_gpu_index_bytes(const ph_gpu_index* ix, const uint8_t* key, size_t len, int minimal,
+                       uint64_t* out) {
+    if (!ix || !out || (!key && len)) return fail(PH_E_INVALID, "null argument");
+    if (ix->info.key_kind != 1) return fail(PH_E_KEYKIND, "string query on a u64-key index");
+    DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    const size_t words = 3 + (len + 7) / 8;  // offsets[2], out, bytes
+    uint64_t* d = nullptr;
+    PH_CUDA(cudaMalloc(&d, words * 8));
+    std::vector<uint64_t> h(words, 0);
+    h[1] = len;
+    if (len) std::memcpy(h.data() + 3, key, len);
+    cudaError_t e = cudaMemcpy(d, h.data(), words * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = phg::launch_query_bytes(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                    reinterpret_cast<const uint8_t*>(d + 3), d, 0, d + 2, 8, 1,
+                                    minimal, nullptr, ix->sms);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d + 2, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "index_bytes");
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+// ph_bench.cu — measurement tools for bench.py and the GPU tests (NOT the product).
+//
+//  * synthetic query streams generated on the device (the workloads of
+//    SURVEY §8d): corpus_u64 keys (reference corpus.hpp:14-16) in a seeded
+//    Feistel-permuted order, or sampled with replacement;
+//  * the random-sector gather microbenchmark that defines R_gather(F), the
+//    pilot-gather roofline, using the same load instruction
+//    and cache policy as the query kernel;
+//  * a bijection checker (bitset + atomicOr old-bit detection).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t corpus_u64(uint64_t i, uint64_t gen_seed) {
+    return mix64(gen_seed + (i + 1) * kGolden);
+}
+// Same function as oracle/ph_oracle.c pho_feistel_perm.
+__host__ __device__ __forceinline__ uint64_t feistel(uint64_t i, uint64_t n, uint64_t seed,
+                                                     unsigned h) {
+    const uint64_t mask = (1ULL << h) - 1;
+    uint64_t x = i;
+    do {
+        uint64_t L = x >> h, R = x & mask;
+#pragma unroll
+        for (uint64_t r = 0; r < 4; r++) {
+            const uint64_t t = L ^ (mix64(R ^ (seed + (r + 1) * kGolden)) & mask);
+            L = R;
+            R = t;
+        }
+        x = (L << h) | R;
+    } while (x >= n);
+    return x;
+}
+unsigned feistel_half_bits(uint64_t n) {
+    unsigned bits = 2;
+    while (bits < 64 && (1ULL << bits) < n) bits += 2;
+    return bits / 2;
+}
+
+__global__ void k_gen_perm(uint64_t* out, uint64_t start, uint64_t count, uint64_t n,
+                           uint64_t gen_seed, uint64_t perm_seed, unsigned h) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = corpus_u64(feistel(start + i, n, perm_seed, h), gen_seed);
+}
+__global__ void k_gen_sample(uint64_t* out, uint64_t start, uint64_t count, uint64_t n,
+                             uint64_t gen_seed, uint64_t sample_seed) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = corpus_u64(mix64(sample_seed + (start + i + 1) * kGolden) % n, gen_seed);
+}
+__global__ void k_gen_corpus(uint64_t* out, uint64_t start, uint64_t count, uint64_t gen_seed) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = corpus_u64(start + i, gen_seed);
+}
+
+// Uniform random 1-byte loads over [0, F): KPT independent loads per thread in
+// flight, the query kernel's ld.global.nc + L2::evict_last policy.
+template <int KPT>
+__global__ void __launch_bounds__(256) k_gather(const uint8_t* __restrict__ buf, uint64_t F,
+                                                uint64_t nloads, uint64_t seed, uint32_t* sink) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * KPT;
+    uint32_t acc = 0;
+    for (uint64_t base = tid * KPT; base < nloads; base += stride) {
+        uint32_t v[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const uint64_t r = mix64(seed + (base + j) * kGolden);
+            const uint64_t a = __umul64hi(r, F);
+            uint16_t x = 0;
+            if (base + j < nloads)
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+                             : "=h"(x) : "l"(buf + a), "l"(pol));
+            v[j] = x;
+        }
+#pragma unroll
+        for (int j = 0; j < KPT; j++) acc += v[j];
+    }
+    if (acc == 0x7fffffffu) *sink = acc;  // keep the loads alive
+}
+
+__global__ void k_bijection(const uint32_t* __restrict__ out, uint64_t count, uint64_t n,
+                            unsigned int* bits, unsigned long long* bad) {
+    unsigned long long local_oob = 0, local_dup = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = out[i];
+        if (v >= n) {
+            local_oob++;
+            continue;
+        }
+        const unsigned int m = 1u << (v & 31);
+        const unsigned int old = atomicOr(bits + (v >> 5), m);
+        if (old & m) local_dup++;
+    }
+    if (local_oob) atomicAdd(bad, local_oob);
+    if (local_dup) atomicAdd(bad + 1, local_dup);
+}
+
+int grid(uint64_t count) {
+    const uint64_t b = (count + 255) / 256;
+    return (int)(b < 148ull * 32 ? (b ? b : 1) : 148ull * 32);
+}
+
+}  // namespace
+
+extern "C" {
+
+int phb_gen_queries_perm(uint64_t* d_out, uint64_t start, uint64_t count, uint64_t n,
+                         uint64_t gen_seed, uint64_t perm_seed, void* stream) {
+    k_gen_perm<<<grid(count), 256, 0, (cudaStream_t)stream>>>(d_out, start, count, n, gen_seed,
+                                                             perm_seed, feistel_half_bits(n));
+    return (int)cudaGetLastError();
+}
+int phb_gen_queries_sample(uint64_t* d_out, uint64_t start, uint64_t count, uint64_t n,
+                           uint64_t gen_seed, uint64_t sample_seed, void* stream) {
+    k_gen_sample<<<grid(count), 256, 0, (cudaStream_t)stream>>>(d_out, start, count, n, gen_seed,
+                                                               sample_seed);
+    return (int)cudaGetLastError();
+}
+int phb_gen_corpus(uint64_t* d_out, uint64_t start, uint64_t count, uint64_t gen_seed,
+                   void* stream) {
+    k_gen_corpus<<<grid(count), 256, 0, (cudaStream_t)stream>>>(d_out, start, count, gen_seed);
+    return (int)cudaGetLastError();
+}
+// host-side twin of k_gen_perm (for building host key arrays without a GPU)
+uint64_t phb_perm_key_host(uint64_t i, uint64_t n, uint64_t gen_seed, uint64_t perm_seed) {
+    return corpus_u64(feistel(i, n, perm_seed, feistel_half_bits(n)), gen_seed);
+}
+
+int phb_gather(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t seed, int kpt,
+               int blocks_per_sm, uint32_t* d_sink, void* stream) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms * (blocks_per_sm > 0 ? blocks_per_sm : 8);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (kpt) {
+        case 1: k_gather<1><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
+        case 4: k_gather<4><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
+        case 16: k_gather<16><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
+        default: k_gather<8><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
+    }
+    return (int)cudaGetLastError();
+}
+
+// bits: ceil(n/32) zeroed u32 words; bad[0] = out-of-range count, bad[1] = duplicates.
+int phb_bijection(const uint32_t* d_out, uint64_t count, uint64_t n, unsigned int* d_bits,
+                  unsigned long long* d_bad, void* stream) {
+    k_bijection<<<grid(count), 256, 0, (cudaStream_t)stream>>>(d_out, count, n, d_bits, d_bad);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+// ph_device.cuh — device-side arithmetic of the PtrHash query path (sm_100a).
+//
+// Bit-exact restatements of the reference's query arithmetic
+// (/root/reference/proj, C++), written for the GPU integer pipes:
+//   hash_int / hash_pilot        include/ptrhash/hash.hpp:27-32
+//   gamma (5 bucket functions)   include/ptrhash/bucket_fn.hpp:18-58, src/bucket_fn.cpp:49-56
+//   part_and_bucket              include/ptrhash/bucket_fn.hpp:66-72
+//   Reducer / FastModU64         include/ptrhash/reduce.hpp:27-77
+//   slot_of / remap_slot         include/ptrhash/index.hpp:91-100
+//   CacheLineEF get              include/ptrhash/cacheline_ef.hpp:38-42, :58-73, :86-90
+//   plain32 / Elias-Fano get     include/ptrhash/remap.hpp:34-45, src/elias_fano.cpp:51-72
+#pragma once
+
+#include <cstdint>
+
+namespace phg {
+
+constexpr uint64_t kC = 0x517cc1b727220a95ULL;  // hash.hpp:13
+constexpr unsigned kFull = 0xffffffffu;
+
+// Everything a query kernel needs, passed by value as a kernel parameter.
+struct DevIndex {
+    const uint8_t* pilots;        // P*B bytes, byte-identical to the PTRH payload
+    const uint8_t* remap;         // CLEF 64-B blocks or plain u32[] (PTRH payload bytes)
+    const uint64_t* ef_low;       // Elias-Fano pieces (re-aligned from the payload)
+    const uint64_t* ef_high;
+    const uint64_t* ef_samples;
+    const uint64_t* opt_table;    // 65537-entry optimal-gamma table (host computed)
+    uint64_t n, P, S, B, seed;
+    uint64_t magic_hi, magic_lo;  // FastModU64::make(S), reduce.hpp:31-36
+    uint64_t hp_base;             // C * (seed & ~0xff): hash_pilot(p) = hp_base + C*((seed^p)&0xff)
+    uint32_t seed_lo8;
+    int32_t remap_kind;           // 0 plain32, 1 CacheLineEF, 2 Elias-Fano
+    int32_t ef_low_bits;
+    int32_t hash_algo;
+};
+
+// ---------------------------------------------------------------------------
+// cache-policy loads/stores
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// streamed key: read once, do not keep in L1, evict first from L2
+__device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p, uint64_t pol) {
+    uint64_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// the random 1-byte pilot gather: read-only path, keep in L2 ahead of the stream
+__device__ __forceinline__ uint32_t ld_gather_u8(const uint8_t* p, uint64_t pol) {
+    uint16_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_stream(uint32_t* p, uint64_t v) {
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"((uint32_t)v) : "memory");
+}
+__device__ __forceinline__ void st_stream(uint64_t* p, uint64_t v) {
+    asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// 64-bit integer helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// ((u128)a * b) >> s for 0 < s < 64
+__device__ __forceinline__ uint64_t mul_shr(uint64_t a, uint64_t b, int s) {
+    return (a * b >> s) | (__umul64hi(a, b) << (64 - s));
+}
+
+// ---------------------------------------------------------------------------
+// bucket functions gamma, bucket_fn.hpp:18-58
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ uint64_t gamma(uint64_t x, const uint64_t* __restrict__ opt) {
+    if constexpr (G == 0) {  // linear :20
+        return x;
+    } else if constexpr (G == 1) {  // quadratic :22
+        return mulhi(x, x);
+    } else if constexpr (G == 2) {  // cubic :27-32: ((x2+x3)>>1)*255>>8 + x>>8, exact
+        const uint64_t x2 = mulhi(x, x);
+        const uint64_t x3 = mulhi(x2, x);
+        const uint64_t half = (x2 >> 1) + (x3 >> 1) + (x2 & x3 & 1);  // floor((x2+x3)/2), no overflow
+        return (half >> 8) * 255 + (((half & 255) * 255) >> 8) + (x >> 8);
+    } else if constexpr (G == 3) {  // skewed :34-39
+        constexpr uint64_t SX = 0x9999999999999999ULL;  // floor(3*2^64/5)
+        constexpr uint64_t SY = 0x4ccccccccccccccc;     // floor(3*2^64/10)
+        if (x < SX) return x >> 1;
+        return SY + mul_shr(x - SX, 7, 2);
+    } else {  // optimal, bucket_fn.cpp:49-56: table interpolation (table uploaded from host)
+        const uint64_t idx = x >> 48;
+        const uint64_t frac = x & ((1ULL << 48) - 1);
+        const uint64_t lo = __ldg(opt + idx);
+        const uint64_t hi = __ldg(opt + idx + 1);
+        return lo + mul_shr(hi - lo, frac, 48);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// reduce, reduce.hpp:38-43 / :67-70
+// ---------------------------------------------------------------------------
+template <bool POW2>
+__device__ __forceinline__ uint64_t reduce(const DevIndex& ix, uint64_t y) {
+    if constexpr (POW2) {
+        return mulhi(kC, y) & (ix.S - 1);
+    } else {
+        // FastModU64::mod: lb = M*y mod 2^128; r = hi64(lb * S) (S < 2^32)
+        const uint64_t lb_lo = ix.magic_lo * y;
+        const uint64_t lb_hi = ix.magic_hi * y + mulhi(ix.magic_lo, y);
+        const uint64_t t1 = mulhi(lb_lo, ix.S);
+        const uint64_t lo = lb_hi * ix.S;
+        return mulhi(lb_hi, ix.S) + ((lo + t1) < t1 ? 1 : 0);
+    }
+}
+
+__device__ __forceinline__ uint64_t hash_pilot(const DevIndex& ix, uint32_t pilot) {
+    // C*(pilot ^ seed) == C*(seed & ~0xff) + C*((seed ^ pilot) & 0xff)  (mod 2^64)
+    return ix.hp_base + kC * (uint64_t)((ix.seed_lo8 ^ pilot) & 0xffu);
+}
+
+// ---------------------------------------------------------------------------
+// remap decodes (rare path: slot >= n)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t select32(uint32_t w, uint32_t rank) {
+    return __fns(w, 0, (int)rank + 1);  // rank-th (0-based) set bit
+}
+
+// CacheLineEF, cacheline_ef.hpp:86-90; block layout :58-73 (offset u32 LE @0,
+// 128-bit mask LE @4, low bytes @20)
+__device__ __forceinline__ uint64_t clef_get(const uint8_t* __restrict__ remap, uint64_t idx) {
+    const uint32_t blk = (uint32_t)(idx / 44);
+    const uint32_t i = (uint32_t)(idx - (uint64_t)blk * 44);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(remap + (uint64_t)blk * 64);
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(w));  // off, m0, m1, m2
+    const uint32_t m3 = __ldg(w + 4);
+    const uint32_t low = __ldg(remap + (uint64_t)blk * 64 + 20 + i);
+    uint32_t r = i, pos;
+    const uint32_t c0 = __popc(a.y);
+    if (r < c0) {
+        pos = select32(a.y, r);
+    } else {
+        r -= c0;
+        const uint32_t c1 = __popc(a.z);
+        if (r < c1) {
+            pos = 32 + select32(a.z, r);
+        } else {
+            r -= c1;
+            const uint32_t c2 = __popc(a.w);
+            pos = (r < c2) ? 64 + select32(a.w, r) : 96 + select32(m3, r - c2);
+        }
+    }
+    return ((uint64_t)a.x << 8) + ((uint64_t)(pos - i) << 8) + low;
+}
+
+__device__ __forceinline__ uint32_t select64(uint64_t w, uint32_t rank) {
+    const uint32_t lo = (uint32_t)w;
+    const uint32_t c = __popc(lo);
+    return rank < c ? select32(lo, rank) : 32 + select32((uint32_t)(w >> 32), rank - c);
+}
+
+// Elias-Fano, elias_fano.cpp:51-72 (samples pack word<<16 | in-word rank)
+__device__ __forceinline__ uint64_t ef_get(const DevIndex& ix, uint64_t i) {
+    const uint64_t sample = ix.ef_samples[i / 512];
+    uint64_t word = sample >> 16;
+    uint32_t want = (uint32_t)(sample & 0xffff) + (uint32_t)(i % 512);
+    for (;;) {
+        const uint32_t c = __popcll(ix.ef_high[word]);
+        if (want < c) break;
+        want -= c;
+        word++;
+    }
+    const uint64_t pos = word * 64 + select64(ix.ef_high[word], want);
+    const uint32_t l = (uint32_t)ix.ef_low_bits;
+    uint64_t low = 0;
+    if (l) {
+        const uint64_t bitpos = i * l;
+        low = ix.ef_low[bitpos / 64] >> (bitpos % 64);
+        if (bitpos % 64 + l > 64) low |= ix.ef_low[bitpos / 64 + 1] << (64 - bitpos % 64);
+        low &= (1ULL << l) - 1;
+    }
+    return ((pos - i) << l) | low;
+}
+
+// RemapTable::get, remap.hpp:34-45 (kind is warp-uniform)
+__device__ __forceinline__ uint64_t remap_get(const DevIndex& ix, uint64_t idx) {
+    if (ix.remap_kind == 1) return clef_get(ix.remap, idx);
+    if (ix.remap_kind == 0) return __ldg(reinterpret_cast<const uint32_t*>(ix.remap) + idx);
+    return ef_get(ix, idx);
+}
+
+}  // namespace phg

@@ -1,0 +1,188 @@
+// ph_query.cu — the bulk query kernels (sm_100a).
+//
+// One kernel answers a batch of keys exactly as PtrHashIndex::index_loop /
+// index_stream / index_batched do (/root/reference/proj/src/index.cpp:15-137):
+//   out[i] = minimal ? remap_slot(slot_of(hash(keys[i]))) : slot_of(hash(keys[i]))
+//
+// Work decomposition: a warp owns a tile of 32*KPT consecutive
+// keys; lane l handles keys tile + j*32 + l for j < KPT, so every key load and
+// every output store is one coalesced 256-B / 128-B warp access. Per thread,
+// all KPT pilot addresses are computed first and the KPT independent 1-byte
+// gathers are issued back to back before any is consumed: this is the GPU's
+// version of the CPU's prefetch ring (index.cpp:101-135), with
+// KPT * (resident warps) gathers in flight per SM. The rare slot >= n keys
+// (~1%) are compacted across the warp with __ballot_sync so one convergent
+// round of remap decodes serves the whole tile.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "ph_device.cuh"
+#include "ph_kernels.h"
+
+namespace phg {
+
+#ifndef PH_KPT
+#define PH_KPT 8
+#endif
+
+// Warp-cooperative remap of the keys flagged in need[] (slot >= n).
+// Entries are ranked across (j, lane) with ballots; lane r of a round decodes
+// entry base+r; results return to their owners with shuffles.
+template <int KPT, class OutT>
+__device__ __forceinline__ void remap_tile(const DevIndex& ix, const bool (&need)[KPT],
+                                           uint64_t (&slot)[KPT]) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1;
+    unsigned m[KPT];
+    unsigned cum[KPT];
+    unsigned total = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+        m[j] = __ballot_sync(kFull, need[j]);
+        cum[j] = total;
+        total += __popc(m[j]);
+    }
+    if (total == 0) return;  // warp-uniform
+    for (unsigned base = 0; base < total; base += 32) {
+        const unsigned r = base + lane;
+        // gather the slot of entry r from its owner (j, src)
+        uint64_t my = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const unsigned cnt = __popc(m[j]);
+            const bool mine = r >= cum[j] && r < cum[j] + cnt;
+            const unsigned src = mine ? __fns(m[j], 0, (int)(r - cum[j]) + 1) : 0;
+            const uint64_t v = __shfl_sync(kFull, slot[j], src & 31);
+            if (mine) my = v;
+        }
+        uint64_t val = 0;
+        if (r < total) val = remap_get(ix, my - ix.n);
+        // hand results back
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const unsigned rr = cum[j] + __popc(m[j] & lt_mask);
+            const uint64_t v = __shfl_sync(kFull, val, (rr - base) & 31);
+            if (need[j] && rr >= base && rr < base + 32) slot[j] = v;
+        }
+    }
+}
+
+template <int G, bool POW2, class OutT, int KPT>
+__global__ void __launch_bounds__(256) k_query_u64(const DevIndex ix,
+                                                   const uint64_t* __restrict__ keys,
+                                                   OutT* __restrict__ out, uint64_t nkeys,
+                                                   int minimal) {
+    constexpr uint64_t kTile = 32ull * KPT;
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+
+    for (uint64_t base = warp * kTile; base < nkeys; base += nwarps * kTile) {
+        const bool full = base + kTile <= nkeys;
+        uint64_t h[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const uint64_t i = base + (uint64_t)j * 32 + lane;
+            const uint64_t k = (full || i < nkeys) ? ld_stream_u64(keys + i, pol_stream) : 0;
+            h[j] = kC * (k ^ ix.seed);  // hash_int, hash.hpp:27 (hi == lo)
+        }
+        uint64_t part[KPT];
+        uint32_t pilot[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            // part_and_bucket, bucket_fn.hpp:66-72
+            part[j] = mulhi(ix.P, h[j]);
+            const uint64_t x = ix.P * h[j];
+            const uint64_t bucket = mulhi(ix.B, gamma<G>(x, ix.opt_table));
+            pilot[j] = ld_gather_u8(ix.pilots + part[j] * ix.B + bucket, pol_keep);
+        }
+        uint64_t slot[KPT];
+        bool need[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            // slot_of, index.hpp:91-96
+            slot[j] = part[j] * ix.S + reduce<POW2>(ix, h[j] ^ hash_pilot(ix, pilot[j]));
+            const uint64_t i = base + (uint64_t)j * 32 + lane;
+            need[j] = minimal && slot[j] >= ix.n && (full || i < nkeys);
+        }
+        if (minimal) remap_tile<KPT, OutT>(ix, need, slot);  // remap_slot, index.hpp:98-100
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const uint64_t i = base + (uint64_t)j * 32 + lane;
+            if (full || i < nkeys) st_stream(out + i, slot[j]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launch plumbing
+// ---------------------------------------------------------------------------
+static std::atomic<uint64_t> g_launches{0};
+static int g_threads_override = 0;
+static int g_bps_override = 0;
+
+uint64_t launch_count() { return g_launches.load(); }
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void set_launch(int threads, int bps) {
+    g_threads_override = threads;
+    g_bps_override = bps;
+}
+
+template <class K>
+static int grid_for(K kernel, int threads, uint64_t work_items_per_block, uint64_t nitems,
+                    int device_sms) {
+    int bps = g_bps_override;
+    if (bps <= 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, threads, 0) != cudaSuccess ||
+            bps <= 0)
+            bps = 1;
+    }
+    const uint64_t want = (nitems + work_items_per_block - 1) / work_items_per_block;
+    const uint64_t cap = (uint64_t)device_sms * (uint64_t)bps;
+    return (int)(want < cap ? (want ? want : 1) : cap);
+}
+
+template <int G, bool POW2, class OutT>
+static cudaError_t launch_u64_t(const DevIndex& ix, const uint64_t* keys, void* out, uint64_t n,
+                                int minimal, cudaStream_t s, int sms) {
+    constexpr int KPT = PH_KPT;
+    auto kern = k_query_u64<G, POW2, OutT, KPT>;
+    const int threads = g_threads_override > 0 ? g_threads_override : 256;
+    const int blocks = grid_for(kern, threads, (uint64_t)threads / 32 * 32 * KPT, n, sms);
+    kern<<<blocks, threads, 0, s>>>(ix, keys, static_cast<OutT*>(out), n, minimal);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+template <class OutT>
+static cudaError_t launch_u64_w(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* k,
+                                void* o, uint64_t n, int minimal, cudaStream_t s, int sms) {
+#define PH_CASE(G)                                                             \
+    case G:                                                                    \
+        return pow2 ? launch_u64_t<G, true, OutT>(ix, k, o, n, minimal, s, sms) \
+                    : launch_u64_t<G, false, OutT>(ix, k, o, n, minimal, s, sms);
+    switch (gamma_kind) {
+        PH_CASE(0)
+        PH_CASE(1)
+        PH_CASE(2)
+        PH_CASE(3)
+        PH_CASE(4)
+    }
+#undef PH_CASE
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
+                             void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
+                             int sms) {
+    if (n == 0) return cudaSuccess;
+    if (out_width == 4)
+        return launch_u64_w<uint32_t>(ix, gamma_kind, pow2, keys, out, n, minimal, s, sms);
+    return launch_u64_w<uint64_t>(ix, gamma_kind, pow2, keys, out, n, minimal, s, sms);
+}
+
+}  // namespace phg

@@ -1,0 +1,306 @@
+// ph_query_bytes.cu — string-key query kernel (sm_100a).
+//
+// Keys are one concatenated byte buffer + u64 offsets[n+1]. Each key is hashed
+// with the index's string hash (hash_bytes, /root/reference/proj/src/hash.cpp:159-193):
+//   kAes64/kAes128   software AESENC/AESENCLAST rounds (T-tables in shared
+//                    memory) reproducing the AES-NI chain of hash.cpp:114-153;
+//   kPortable64/128  the folded-multiply hash of hash.cpp:87-104 / :184-190
+//                    (kFx64 on bytes also uses it, hash.cpp:162-167).
+// then goes through the same slot_of / remap_slot as the u64 path.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ph_device.cuh"
+#include "ph_kernels.h"
+
+namespace phg {
+
+constexpr uint64_t kP1 = 0x8bb84b93962eacc9ULL;  // hash.cpp:83-85
+constexpr uint64_t kP2 = 0x2d358dccaa6c78a5ULL;
+constexpr uint64_t kP3 = 0x4b33a62ed433d4a3ULL;
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+// AES S-box (FIPS-197), used to fill the shared-memory T-tables.
+__constant__ uint8_t c_sbox[256] = {
+    0x63, 0x7c, 0x77, 0x7b, 0xf2, 0x6b, 0x6f, 0xc5, 0x30, 0x01, 0x67, 0x2b, 0xfe, 0xd7, 0xab, 0x76,
+    0xca, 0x82, 0xc9, 0x7d, 0xfa, 0x59, 0x47, 0xf0, 0xad, 0xd4, 0xa2, 0xaf, 0x9c, 0xa4, 0x72, 0xc0,
+    0xb7, 0xfd, 0x93, 0x26, 0x36, 0x3f, 0xf7, 0xcc, 0x34, 0xa5, 0xe5, 0xf1, 0x71, 0xd8, 0x31, 0x15,
+    0x04, 0xc7, 0x23, 0xc3, 0x18, 0x96, 0x05, 0x9a, 0x07, 0x12, 0x80, 0xe2, 0xeb, 0x27, 0xb2, 0x75,
+    0x09, 0x83, 0x2c, 0x1a, 0x1b, 0x6e, 0x5a, 0xa0, 0x52, 0x3b, 0xd6, 0xb3, 0x29, 0xe3, 0x2f, 0x84,
+    0x53, 0xd1, 0x00, 0xed, 0x20, 0xfc, 0xb1, 0x5b, 0x6a, 0xcb, 0xbe, 0x39, 0x4a, 0x4c, 0x58, 0xcf,
+    0xd0, 0xef, 0xaa, 0xfb, 0x43, 0x4d, 0x33, 0x85, 0x45, 0xf9, 0x02, 0x7f, 0x50, 0x3c, 0x9f, 0xa8,
+    0x51, 0xa3, 0x40, 0x8f, 0x92, 0x9d, 0x38, 0xf5, 0xbc, 0xb6, 0xda, 0x21, 0x10, 0xff, 0xf3, 0xd2,
+    0xcd, 0x0c, 0x13, 0xec, 0x5f, 0x97, 0x44, 0x17, 0xc4, 0xa7, 0x7e, 0x3d, 0x64, 0x5d, 0x19, 0x73,
+    0x60, 0x81, 0x4f, 0xdc, 0x22, 0x2a, 0x90, 0x88, 0x46, 0xee, 0xb8, 0x14, 0xde, 0x5e, 0x0b, 0xdb,
+    0xe0, 0x32, 0x3a, 0x0a, 0x49, 0x06, 0x24, 0x5c, 0xc2, 0xd3, 0xac, 0x62, 0x91, 0x95, 0xe4, 0x79,
+    0xe7, 0xc8, 0x37, 0x6d, 0x8d, 0xd5, 0x4e, 0xa9, 0x6c, 0x56, 0xf4, 0xea, 0x65, 0x7a, 0xae, 0x08,
+    0xba, 0x78, 0x25, 0x2e, 0x1c, 0xa6, 0xb4, 0xc6, 0xe8, 0xdd, 0x74, 0x1f, 0x4b, 0xbd, 0x8b, 0x8a,
+    0x70, 0x3e, 0xb5, 0x66, 0x48, 0x03, 0xf6, 0x0e, 0x61, 0x35, 0x57, 0xb9, 0x86, 0xc1, 0x1d, 0x9e,
+    0xe1, 0xf8, 0x98, 0x11, 0x69, 0xd9, 0x8e, 0x94, 0x9b, 0x1e, 0x87, 0xe9, 0xce, 0x55, 0x28, 0xdf,
+    0x8c, 0xa1, 0x89, 0x0d, 0xbf, 0xe6, 0x42, 0x68, 0x41, 0x99, 0x2d, 0x0f, 0xb0, 0x54, 0xbb, 0x16};
+
+struct AesTables {
+    uint32_t t[4][256];  // MixColumns∘SubBytes columns, rotated per row
+    uint32_t s[256];     // plain S-box (aesenclast)
+};
+
+__device__ __forceinline__ uint8_t xtime(uint8_t a) {
+    return (uint8_t)((a << 1) ^ ((a & 0x80) ? 0x1b : 0));
+}
+
+__device__ void fill_tables(AesTables& T) {
+    for (int x = threadIdx.x; x < 256; x += blockDim.x) {
+        const uint8_t s = c_sbox[x];
+        const uint8_t s2 = xtime(s), s3 = (uint8_t)(s2 ^ s);
+        const uint32_t t0 = (uint32_t)s2 | ((uint32_t)s << 8) | ((uint32_t)s << 16) | ((uint32_t)s3 << 24);
+        T.t[0][x] = t0;
+        T.t[1][x] = __funnelshift_l(t0, t0, 8);
+        T.t[2][x] = __funnelshift_l(t0, t0, 16);
+        T.t[3][x] = __funnelshift_l(t0, t0, 24);
+        T.s[x] = s;
+    }
+}
+
+// state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
+// in-memory byte order of the __m128i in hash.cpp. AESENC = ShiftRows,
+// SubBytes, MixColumns, AddRoundKey (Intel semantics).
+__device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4],
+                                       const AesTables& T) {
+    uint32_t o[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        o[c] = T.t[0][s[c] & 0xff] ^ T.t[1][(s[(c + 1) & 3] >> 8) & 0xff] ^
+               T.t[2][(s[(c + 2) & 3] >> 16) & 0xff] ^ T.t[3][s[(c + 3) & 3] >> 24] ^ k[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c++) s[c] = o[c];
+}
+__device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)[4],
+                                           const AesTables& T) {
+    uint32_t o[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        o[c] = (T.s[s[c] & 0xff] | (T.s[(s[(c + 1) & 3] >> 8) & 0xff] << 8) |
+                (T.s[(s[(c + 2) & 3] >> 16) & 0xff] << 16) | (T.s[s[(c + 3) & 3] >> 24] << 24)) ^
+               k[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c++) s[c] = o[c];
+}
+
+// Loads min(avail,16) bytes at base+off as 4 LE words, zero past `avail`.
+// Only aligned 4-byte words that hold at least one requested byte are read,
+// so no access leaves the 4-byte words covering the key.
+__device__ __forceinline__ void load16(const uint8_t* __restrict__ base, uint64_t off,
+                                       uint32_t avail, uint32_t (&w)[4]) {
+    const uint64_t a = off & ~3ull;
+    const uint32_t sh = (uint32_t)(off & 3) * 8;
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(base + a);
+    const uint64_t end = off + (avail < 16 ? avail : 16);
+    uint32_t r[5];
+#pragma unroll
+    for (int t = 0; t < 5; t++) r[t] = (a + 4 * t < end) ? __ldg(p + t) : 0u;
+#pragma unroll
+    for (int t = 0; t < 4; t++) w[t] = __funnelshift_r(r[t], r[t + 1], sh);
+    if (avail < 16) {
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int keep = (int)avail - 4 * t;  // bytes to keep in word t
+            if (keep <= 0) w[t] = 0;
+            else if (keep < 4) w[t] &= (1u << (8 * keep)) - 1;
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t mum(uint64_t a, uint64_t b) {  // hash.cpp:53-56
+    return (a * b) ^ __umul64hi(a, b);
+}
+
+__device__ __forceinline__ uint64_t w64(const uint32_t (&w)[4], int i) {
+    return (uint64_t)w[2 * i] | ((uint64_t)w[2 * i + 1] << 32);
+}
+
+// portable_hash64, hash.cpp:87-104 (read_tail :71-81)
+__device__ uint64_t portable_hash64(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
+                                    uint64_t seed) {
+    uint64_t acc = seed ^ mum((uint64_t)len ^ kP1, seed ^ kP2);
+    uint32_t i = 0;
+    uint32_t w[4];
+    while (i + 16 <= len) {
+        load16(data, off + i, 16, w);
+        acc = mum(w64(w, 0) ^ kP1, w64(w, 1) ^ acc);
+        i += 16;
+    }
+    uint64_t a = 0, b = 0;
+    const uint32_t rem = len - i;
+    if (rem > 0) {
+        load16(data, off + i, rem, w);  // the remaining 1..15 bytes, zero padded
+        auto tail = [&](uint32_t start, uint32_t m) -> uint64_t {  // read_tail(p+start, m)
+            auto byte_at = [&](uint32_t q) -> uint64_t { return (w[q >> 2] >> (8 * (q & 3))) & 0xff; };
+            if (m >= 4) {
+                uint64_t lo = 0, hi = 0;
+                for (int t = 0; t < 4; t++) {
+                    lo |= byte_at(start + t) << (8 * t);
+                    hi |= byte_at(start + m - 4 + t) << (8 * t);
+                }
+                return lo | (hi << 32);
+            }
+            return byte_at(start) | (byte_at(start + (m >> 1)) << 8) | (byte_at(start + m - 1) << 16);
+        };
+        if (rem > 8) {
+            a = w64(w, 0);
+            b = tail(8, rem - 8);
+        } else {
+            a = tail(0, rem);
+        }
+    }
+    acc = mum(a ^ kP2 ^ (uint64_t)len, b ^ acc ^ kP3);
+    return mum(acc, acc ^ kP1);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // common.hpp:54-58
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ void set128(uint32_t (&s)[4], uint64_t hi, uint64_t lo) {
+    s[0] = (uint32_t)lo;
+    s[1] = (uint32_t)(lo >> 32);
+    s[2] = (uint32_t)hi;
+    s[3] = (uint32_t)(hi >> 32);
+}
+
+// aes_core + aes_hash, hash.cpp:114-153
+__device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
+                         uint64_t seed, bool wide, const AesTables& T, uint64_t& hi,
+                         uint64_t& lo) {
+    uint32_t k0[4], k1[4], s[4], w[4];
+    set128(k0, seed ^ kP1, seed + kGolden);
+    set128(k1, mix64(seed) ^ kP2, (~seed) * 0x6c62272e07bb0143ULL);
+    set128(s, (uint64_t)len * kC, seed ^ (uint64_t)len);
+    aesenc(s, k0, T);
+    uint32_t i = 0;
+    while (i + 16 <= len) {
+        load16(data, off + i, 16, w);
+#pragma unroll
+        for (int c = 0; c < 4; c++) s[c] ^= w[c];
+        aesenc(s, k1, T);
+        i += 16;
+    }
+    if (i < len) {
+        const uint32_t rem = len - i;
+        load16(data, off + i, rem, w);
+        w[3] ^= rem << 24;  // buf[15] ^= len - i
+#pragma unroll
+        for (int c = 0; c < 4; c++) s[c] ^= w[c];
+        aesenc(s, k1, T);
+    }
+    aesenc(s, k0, T);
+    aesenc(s, k1, T);
+    aesenclast(s, k0, T);
+    const uint64_t l = (uint64_t)s[0] | ((uint64_t)s[1] << 32);
+    const uint64_t h = (uint64_t)s[2] | ((uint64_t)s[3] << 32);
+    if (!wide) {
+        hi = lo = h ^ (l * kC);
+    } else {
+        hi = h;
+        lo = l;
+    }
+}
+
+template <int G, bool POW2, class OutT>
+__global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
+                                                     const uint8_t* __restrict__ data,
+                                                     const uint64_t* __restrict__ offsets,
+                                                     uint64_t base_off, OutT* __restrict__ out, uint64_t nkeys,
+                                                     int minimal) {
+    __shared__ AesTables T;
+    const int algo = ix.hash_algo;
+    if (algo == 1 || algo == 2) {
+        fill_tables(T);
+        __syncthreads();
+    }
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t pol_keep = policy_evict_last();
+    // Grid-stride with whole-warp iterations so the remap ballot stays convergent.
+    const uint64_t nround = (nkeys + stride - 1) / stride;
+    for (uint64_t r = 0; r < nround; r++) {
+        const uint64_t i = r * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        const bool valid = i < nkeys;
+        uint64_t hi = 0, lo = 0;
+        if (valid) {
+            const uint64_t o0 = __ldg(offsets + i) - base_off, o1 = __ldg(offsets + i + 1) - base_off;
+            const uint32_t len = (uint32_t)(o1 - o0);
+            if (algo == 1 || algo == 2) {
+                aes_hash(data, o0, len, ix.seed, algo == 2, T, hi, lo);
+            } else if (algo == 4) {
+                hi = portable_hash64(data, o0, len, ix.seed ^ kP3);
+                lo = portable_hash64(data, o0, len, mix64(ix.seed) + kGolden);
+            } else {
+                hi = lo = portable_hash64(data, o0, len, ix.seed);
+            }
+        }
+        const uint64_t part = mulhi(ix.P, hi);
+        const uint64_t bucket = mulhi(ix.B, gamma<G>(ix.P * hi, ix.opt_table));
+        const uint32_t pilot = valid ? ld_gather_u8(ix.pilots + part * ix.B + bucket, pol_keep) : 0;
+        uint64_t slot[1] = {part * ix.S + reduce<POW2>(ix, lo ^ hash_pilot(ix, pilot))};
+        if (minimal) {
+            const bool need = valid && slot[0] >= ix.n;
+            if (__any_sync(kFull, need)) {
+                // rare path: every flagged lane decodes (one convergent round per warp)
+                uint64_t v = 0;
+                if (need) v = remap_get(ix, slot[0] - ix.n);
+                if (need) slot[0] = v;
+            }
+        }
+        if (valid) st_stream(out + i, slot[0]);
+    }
+}
+
+template <int G, bool POW2, class OutT>
+static cudaError_t launch_b(const DevIndex& ix, const uint8_t* d, const uint64_t* o,
+                            uint64_t bo, void* out, uint64_t n, int minimal, cudaStream_t s, int sms) {
+    auto kern = k_query_bytes<G, POW2, OutT>;
+    int bps = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0) != cudaSuccess || bps <= 0)
+        bps = 1;
+    const uint64_t want = (n + 255) / 256;
+    const uint64_t cap = (uint64_t)sms * bps;
+    const int blocks = (int)(want < cap ? want : cap);
+    kern<<<blocks, 256, 0, s>>>(ix, d, o, bo, static_cast<OutT*>(out), n, minimal);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <class OutT>
+static cudaError_t launch_bw(const DevIndex& ix, int g, bool pow2, const uint8_t* d,
+                             const uint64_t* o, uint64_t bo, void* out, uint64_t n, int minimal, cudaStream_t s,
+                             int sms) {
+#define PH_CASE(G)                                                                 \
+    case G:                                                                        \
+        return pow2 ? launch_b<G, true, OutT>(ix, d, o, bo, out, n, minimal, s, sms) \
+                    : launch_b<G, false, OutT>(ix, d, o, bo, out, n, minimal, s, sms);
+    switch (g) {
+        PH_CASE(0)
+        PH_CASE(1)
+        PH_CASE(2)
+        PH_CASE(3)
+        PH_CASE(4)
+    }
+#undef PH_CASE
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_query_bytes(const DevIndex& ix, int gamma_kind, bool pow2,
+                               const uint8_t* bytes, const uint64_t* offsets, uint64_t base_off,
+                               void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
+                               int sms) {
+    if (n == 0) return cudaSuccess;
+    if (out_width == 4)
+        return launch_bw<uint32_t>(ix, gamma_kind, pow2, bytes, offsets, base_off, out, n, minimal, s, sms);
+    return launch_bw<uint64_t>(ix, gamma_kind, pow2, bytes, offsets, base_off, out, n, minimal, s, sms);
+}
+
+}  // namespace phg

@@ -105,6 +105,10 @@ int ph_gpu_index_bytes(const ph_gpu_index* index, const uint8_t* key, size_t len
 uint64_t ph_gpu_launch_count(void);
 /* Override the bulk-kernel launch shape (0 = automatic). For tuning/bench. */
 int ph_gpu_set_launch(int threads_per_block, int blocks_per_sm);
+/* L2 residency budget for the pilot gather (default: all pilots): the first hot_bytes/P pilot
+ * bytes of every part are loaded with L2::evict_last, all other pilot loads with
+ * L2::evict_first. Tuning knob; do not call while queries on `index` are in flight. */
+int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes);
 
 #ifdef __cplusplus
 }

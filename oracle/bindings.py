@@ -283,6 +283,38 @@ class Port:
         L.pho_query_bytes.argtypes = [C.POINTER(PhoIndex), u8p, u64p, C.c_size_t, u64p, C.c_int]
         L.pho_feistel_perm.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
         L.pho_feistel_perm.restype = C.c_uint64
+        L.pho_gen_corpus.argtypes = [u64p, C.c_uint64, C.c_uint64, C.c_uint64]
+        L.pho_gen_perm_keys.argtypes = [u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                        C.c_uint64]
+        L.pho_gen_sample_keys.argtypes = list(L.pho_gen_perm_keys.argtypes)
+
+    def gen_keys(self, kind: str, start: int, count: int, n: int, gen_seed: int, seed: int = 0,
+                 threads: int = 0) -> np.ndarray:
+        """Host generation of the synthetic key streams ("corpus", "perm", "sample"), threaded."""
+        import threading
+        out = np.empty(count, dtype=np.uint64)
+        T = threads or (os.cpu_count() or 1)
+        step = (count + T - 1) // T
+
+        def work(t):
+            b = t * step
+            m = min(step, count - b)
+            if m <= 0:
+                return
+            ptr = out[b:].ctypes.data_as(u64p)
+            if kind == "corpus":
+                self.L.pho_gen_corpus(ptr, start + b, m, gen_seed)
+            elif kind == "perm":
+                self.L.pho_gen_perm_keys(ptr, start + b, m, n, gen_seed, seed)
+            else:
+                self.L.pho_gen_sample_keys(ptr, start + b, m, n, gen_seed, seed)
+
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(T)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        return out
 
     def hash_bytes(self, b: bytes, seed: int, algo: int):
         arr = (C.c_uint8 * max(1, len(b))).from_buffer_copy(b if b else b"\0")

@@ -462,6 +462,21 @@ uint64_t pho_corpus_u64(uint64_t i, uint64_t gen_seed) {
     return pho_mix64(gen_seed + (i + 1) * kGolden);
 }
 
+/* Bulk host generators for the synthetic workloads (bench.py's reference arm). */
+void pho_gen_corpus(uint64_t* out, uint64_t start, uint64_t count, uint64_t gen_seed) {
+    for (uint64_t i = 0; i < count; i++) out[i] = pho_corpus_u64(start + i, gen_seed);
+}
+void pho_gen_perm_keys(uint64_t* out, uint64_t start, uint64_t count, uint64_t n,
+                       uint64_t gen_seed, uint64_t perm_seed) {
+    for (uint64_t i = 0; i < count; i++)
+        out[i] = pho_corpus_u64(pho_feistel_perm(start + i, n, perm_seed), gen_seed);
+}
+void pho_gen_sample_keys(uint64_t* out, uint64_t start, uint64_t count, uint64_t n,
+                         uint64_t gen_seed, uint64_t sample_seed) {
+    for (uint64_t i = 0; i < count; i++)
+        out[i] = pho_corpus_u64(pho_mix64(sample_seed + (start + i + 1) * kGolden) % n, gen_seed);
+}
+
 /* Seeded permutation of [0,n) used as the "shuffled query order" of the
  * synthetic workloads (ours, not the reference's): a 4-round balanced Feistel
  * network over the smallest even-bit domain >= n, with cycle walking. The GPU

@@ -61,6 +61,11 @@ void pho_query_bytes(const pho_index* ix, const uint8_t* data, const uint64_t* o
 /* ---- synthetic workloads shared with the GPU harness ---- */
 uint64_t pho_corpus_u64(uint64_t i, uint64_t gen_seed);
 uint64_t pho_feistel_perm(uint64_t i, uint64_t n, uint64_t seed);
+void pho_gen_corpus(uint64_t* out, uint64_t start, uint64_t count, uint64_t gen_seed);
+void pho_gen_perm_keys(uint64_t* out, uint64_t start, uint64_t count, uint64_t n,
+                       uint64_t gen_seed, uint64_t perm_seed);
+void pho_gen_sample_keys(uint64_t* out, uint64_t start, uint64_t count, uint64_t n,
+                         uint64_t gen_seed, uint64_t sample_seed);
 
 #ifdef __cplusplus
 }

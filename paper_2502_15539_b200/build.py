@@ -53,7 +53,7 @@ def build_lib(name, sources, extra=(), log=None, force=False):
     srcs = [os.path.join(CSRC, s) for s in sources]
     if not force and not _stale(out, srcs + hdrs):
         return out
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build", os.path.basename(name)[:-3])
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for s in srcs:
@@ -76,6 +76,18 @@ def build_cpp_test(log):
         _run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
               src, "-o", out, "-L", PKG, "-lph_gpu", f"-Wl,-rpath,{PKG}", "-ldl", "-pthread"], log)
     return out
+
+
+def build_variants(defs, log=None, force=False):
+    """Tuning builds of the product with different compile-time knobs (tools/tune.py)."""
+    os.makedirs(os.path.join(PKG, "variants"), exist_ok=True)
+    outs = []
+    for name, flags in defs.items():
+        out = build_lib(os.path.join("variants", f"libph_gpu_{name}.so"),
+                        ["ph_query.cu", "ph_query_bytes.cu", "ph_abi.cu"], extra=flags, log=log,
+                        force=force)
+        outs.append(out)
+    return outs
 
 
 def main(force=False):

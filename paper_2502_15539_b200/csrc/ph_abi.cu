@@ -89,6 +89,16 @@ void optimal_table(std::vector<uint64_t>& t) {
     }
 }
 
+// Pilot bytes loaded with L2::evict_last: the first hot_bytes/P pilot
+// bytes of every part, where the bucket function concentrates the queries.
+constexpr uint64_t kDefaultHotBytes = ~uint64_t{0};  // all pilots evict_last (tools/tune.py sweep)
+
+uint64_t hot_limit_for(uint64_t P, uint64_t B, uint64_t hot_bytes) {
+    if (P == 0) return 0;
+    const uint64_t per_part = hot_bytes / P;
+    return per_part < B ? per_part : B;
+}
+
 }  // namespace
 
 struct ph_gpu_index {
@@ -329,12 +339,19 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
     d.remap_kind = p.remap_kind;
     d.ef_low_bits = p.ef_low_bits;
     d.hash_algo = p.algo;
+    d.hot_limit = hot_limit_for(p.P, p.B, kDefaultHotBytes);
     *out = ix;
     return PH_OK;
 }
 
 int ph_gpu_index_destroy(ph_gpu_index* index) {
     release(index);
+    return PH_OK;
+}
+
+int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes) {
+    if (!index) return fail(PH_E_INVALID, "null index");
+    index->dev.hot_limit = hot_limit_for(index->info.parts, index->info.buckets_per_part, hot_bytes);
     return PH_OK;
 }
 

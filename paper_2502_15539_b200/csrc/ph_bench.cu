@@ -92,6 +92,42 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t* __restrict__ buf,
     if (acc == 0x7fffffffu) *sink = acc;  // keep the loads alive
 }
 
+// Skewed gather: a fraction p_hot (out of 2^32) of the loads go uniformly to [0, F_hot),
+// the rest uniformly to [F_hot, F). policy_mode: 0 = all evict_last, 1 = hot evict_last /
+// cold evict_first, 2 = all normal (no hint).
+__global__ void __launch_bounds__(256) k_gather_skew(const uint8_t* __restrict__ buf,
+                                                     uint64_t F_hot, uint64_t F, uint32_t p_hot,
+                                                     uint64_t nloads, uint64_t seed, int mode,
+                                                     uint32_t* sink) {
+    uint64_t pk, pc;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pk));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pc));
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 8;
+    uint32_t acc = 0;
+    for (uint64_t base = tid * 8; base < nloads; base += stride) {
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t r = mix64(seed + (base + j) * kGolden);
+            const bool hot = (uint32_t)r < p_hot;
+            const uint64_t a = hot ? __umul64hi(r, F_hot) : F_hot + __umul64hi(r, F - F_hot);
+            uint16_t x = 0;
+            if (mode == 2) {
+                asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(x) : "l"(buf + a));
+            } else {
+                const uint64_t pol = (mode == 1 && !hot) ? pc : pk;
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+                             : "=h"(x) : "l"(buf + a), "l"(pol));
+            }
+            v[j] = x;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc += v[j];
+    }
+    if (acc == 0x7fffffffu) *sink = acc;
+}
+
 __global__ void k_bijection(const uint32_t* __restrict__ out, uint64_t count, uint64_t n,
                             unsigned int* bits, unsigned long long* bad) {
     unsigned long long local_oob = 0, local_dup = 0;
@@ -154,6 +190,47 @@ int phb_gather(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t seed,
         default: k_gather<8><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
     }
     return (int)cudaGetLastError();
+}
+
+int phb_gather_skew(const uint8_t* d_buf, uint64_t F_hot, uint64_t F, double p_hot,
+                    uint64_t nloads, uint64_t seed, int mode, uint32_t* d_sink, void* stream) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const uint32_t ph = (uint32_t)(p_hot * 4294967295.0);
+    k_gather_skew<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(d_buf, F_hot, F, ph, nloads, seed,
+                                                            mode, d_sink);
+    return (int)cudaGetLastError();
+}
+
+// Context-wide L2 knobs for the tuning sweeps (tools/tune.py).
+int phb_set_l2_fetch_granularity(int bytes) {
+    return (int)cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes);
+}
+long long phb_get_l2_fetch_granularity() {
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    return (long long)v;
+}
+// Persisting-L2 window on `stream` over [ptr, ptr+bytes) with the given hit ratio;
+// bytes == 0 clears it.
+int phb_set_persist(void* stream, void* ptr, size_t bytes, float hit_ratio, size_t carve) {
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve);
+    if (e != cudaSuccess) return (int)e;
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = ptr;
+    a.accessPolicyWindow.num_bytes = bytes;
+    a.accessPolicyWindow.hitRatio = hit_ratio;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (bytes == 0) a.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+    e = cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &a);
+    if (bytes == 0) cudaCtxResetPersistingL2Cache();
+    return (int)e;
+}
+long long phb_max_persist_bytes() {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, 0);
+    return v;
 }
 
 // bits: ceil(n/32) zeroed u32 words; bad[0] = out-of-range count, bad[1] = duplicates.

@@ -33,6 +33,12 @@ struct DevIndex {
     int32_t remap_kind;           // 0 plain32, 1 CacheLineEF, 2 Elias-Fano
     int32_t ef_low_bits;
     int32_t hash_algo;
+    // L2 residency policy for the pilot gather: buckets whose in-part index is below
+    // hot_limit are loaded with L2::evict_last, the rest with L2::evict_first. The
+    // bucket functions put most keys in the first buckets of every part (cubic gamma:
+    // the first ~10% of each part's pilot bytes serve ~40% of the queries), so the L2
+    // keeps exactly the pilots that are re-read.
+    uint64_t hot_limit;
 };
 
 // ---------------------------------------------------------------------------

@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(256) k_query_u64(const DevIndex ix,
             part[j] = mulhi(ix.P, h[j]);
             const uint64_t x = ix.P * h[j];
             const uint64_t bucket = mulhi(ix.B, gamma<G>(x, ix.opt_table));
-            pilot[j] = ld_gather_u8(ix.pilots + part[j] * ix.B + bucket, pol_keep);
+            pilot[j] = ld_gather_u8(ix.pilots + part[j] * ix.B + bucket,
+                                    bucket < ix.hot_limit ? pol_keep : pol_stream);
         }
         uint64_t slot[KPT];
         bool need[KPT];

@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
     }
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_cold = policy_evict_first();
     // Grid-stride with whole-warp iterations so the remap ballot stays convergent.
     const uint64_t nround = (nkeys + stride - 1) / stride;
     for (uint64_t r = 0; r < nround; r++) {
@@ -244,7 +245,9 @@ __global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
         }
         const uint64_t part = mulhi(ix.P, hi);
         const uint64_t bucket = mulhi(ix.B, gamma<G>(ix.P * hi, ix.opt_table));
-        const uint32_t pilot = valid ? ld_gather_u8(ix.pilots + part * ix.B + bucket, pol_keep) : 0;
+        const uint32_t pilot = valid ? ld_gather_u8(ix.pilots + part * ix.B + bucket,
+                                                  bucket < ix.hot_limit ? pol_keep : pol_cold)
+                                   : 0;
         uint64_t slot[1] = {part * ix.S + reduce<POW2>(ix, lo ^ hash_pilot(ix, pilot))};
         if (minimal) {
             const bool need = valid && slot[0] >= ix.n;

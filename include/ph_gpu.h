@@ -105,10 +105,13 @@ int ph_gpu_index_bytes(const ph_gpu_index* index, const uint8_t* key, size_t len
 uint64_t ph_gpu_launch_count(void);
 /* Override the bulk-kernel launch shape (0 = automatic). For tuning/bench. */
 int ph_gpu_set_launch(int threads_per_block, int blocks_per_sm);
-/* L2 residency budget for the pilot gather (default: all pilots): the first hot_bytes/P pilot
- * bytes of every part are loaded with L2::evict_last, all other pilot loads with
- * L2::evict_first. Tuning knob; do not call while queries on `index` are in flight. */
-int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes);
+/* Pilot-gather L2 policy (default: hot_bytes = 64 MiB, flags = 0). The device copy of
+ * the pilots is laid out hot-first: the first hot_bytes/P buckets of every part form a
+ * contiguous region covered by a persisting L2 access-policy window (this sets the
+ * context's cudaLimitPersistingL2CacheSize). flags: 1 = cold-region loads use
+ * L2::evict_first, 2 = no persisting window. Results are unaffected. Tuning knob: do not
+ * call while queries on `index` are in flight. */
+int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flags);
 
 #ifdef __cplusplus
 }

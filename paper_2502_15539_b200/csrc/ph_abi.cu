@@ -89,15 +89,13 @@ void optimal_table(std::vector<uint64_t>& t) {
     }
 }
 
-// Pilot bytes loaded with L2::evict_last: the first hot_bytes/P pilot
-// bytes of every part, where the bucket function concentrates the queries.
-constexpr uint64_t kDefaultHotBytes = ~uint64_t{0};  // all pilots evict_last (tools/tune.py sweep)
-
-uint64_t hot_limit_for(uint64_t P, uint64_t B, uint64_t hot_bytes) {
-    if (P == 0) return 0;
-    const uint64_t per_part = hot_bytes / P;
-    return per_part < B ? per_part : B;
-}
+// Hot-first pilot layout budget: the first hot_bytes/P pilots of every
+// part go to a contiguous hot region under a persisting L2 window.
+constexpr uint64_t kDefaultHotBytes = uint64_t{64} << 20;
+// ph_gpu_index_set_l2_policy flags
+constexpr int kL2ColdEvictFirst = 1;  // cold-region pilot loads use L2::evict_first
+constexpr int kL2NoWindow = 2;        // no persisting access-policy window
+constexpr int kDefaultL2Flags = 0;
 
 }  // namespace
 
@@ -212,6 +210,52 @@ int upload(const void* src, size_t bytes, void** dst) {
     return PH_OK;
 }
 
+// Uploads the file-order pilots `file` (P*B bytes) in the hot-first layout for
+// `hot_bytes` and sets the persisting-L2 window over the hot region.
+int apply_pilot_layout(ph_gpu_index* ix, const uint8_t* file, uint64_t hot_bytes, int flags) {
+    const uint64_t P = ix->info.parts, B = ix->info.buckets_per_part;
+    const uint64_t total = P * B;
+    uint64_t H = B;
+    if (total > hot_bytes && P > 0) H = hot_bytes / P < B ? hot_bytes / P : B;
+    phg::DevIndex& d = ix->dev;
+    int rc;
+    if (H == B) {
+        rc = upload(file, total, &ix->d_pilots);
+    } else {
+        std::vector<uint8_t> lay(total);
+        for (uint64_t part = 0; part < P; part++) {
+            std::memcpy(lay.data() + part * H, file + part * B, H);
+            std::memcpy(lay.data() + P * H + part * (B - H), file + part * B + H, B - H);
+        }
+        rc = upload(lay.data(), total, &ix->d_pilots);
+    }
+    if (rc) return rc;
+    d.pilots = static_cast<const uint8_t*>(ix->d_pilots);
+    d.hot_b = H;
+    d.cold_b = B - H;
+    d.hot_total = P * H;
+    d.cold_evict_first = (flags & kL2ColdEvictFirst) ? 1 : 0;
+    d.window_bytes = 0;
+    d.window_hit_ratio = 0.f;
+    int max_window = 0, max_persist = 0;
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ix->device);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ix->device);
+    if (!(flags & kL2NoWindow) && max_window > 0 && max_persist > 0 && d.hot_total > 0) {
+        const uint64_t win = d.hot_total < (uint64_t)max_window ? d.hot_total : (uint64_t)max_window;
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        const size_t want = win < (uint64_t)max_persist ? win : (uint64_t)max_persist;
+        if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+            cudaGetLastError();  // persisting L2 unavailable: run without the window
+            return PH_OK;
+        }
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        d.window_bytes = win;
+        d.window_hit_ratio = cur >= win ? 1.f : static_cast<float>(cur) / static_cast<float>(win);
+    }
+    return PH_OK;
+}
+
 void release(ph_gpu_index* ix) {
     if (!ix) return;
     DeviceGuard g(ix->device);
@@ -275,6 +319,10 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
     if (e != cudaSuccess || ndev == 0)
         return fail(PH_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
     if (device < 0 || device >= ndev) return fail(PH_E_INVALID, "bad device ordinal");
+    // The kernels use 32-bit P, B, S products. Every shape compute_shape()
+    // produces for n < 2^32 satisfies this; larger ones are rejected, not mis-answered.
+    if (p.P >= (uint64_t{1} << 32) || p.B >= (uint64_t{1} << 32) || p.S >= (uint64_t{1} << 32))
+        return fail(PH_E_UNSUPPORTED, "shape needs P, B, S < 2^32 on the GPU path");
     DeviceGuard g(device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
 
@@ -297,7 +345,7 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
     I.pow2 = is_pow2(p.S) ? 1 : 0;
     I.device = device;
 
-    int rc = upload(p.pilots, p.pilots_len, &ix->d_pilots);
+    int rc = apply_pilot_layout(ix, p.pilots, kDefaultHotBytes, kDefaultL2Flags);
     if (!rc && p.remap_kind != 2) {
         rc = upload(p.remap, p.remap_len, &ix->d_remap);
         I.remap_bytes = p.remap_len;
@@ -333,13 +381,13 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
         const u128 m = ~u128{0} / p.S + 1;
         d.magic_hi = static_cast<uint64_t>(m >> 64);
         d.magic_lo = static_cast<uint64_t>(m);
+        d.mod_m64 = static_cast<uint64_t>((u128{1} << 64) / p.S);
     }
     d.hp_base = phg::kC * (p.seed & ~uint64_t{0xff});
     d.seed_lo8 = static_cast<uint32_t>(p.seed & 0xff);
     d.remap_kind = p.remap_kind;
     d.ef_low_bits = p.ef_low_bits;
     d.hash_algo = p.algo;
-    d.hot_limit = hot_limit_for(p.P, p.B, kDefaultHotBytes);
     *out = ix;
     return PH_OK;
 }
@@ -349,10 +397,23 @@ int ph_gpu_index_destroy(ph_gpu_index* index) {
     return PH_OK;
 }
 
-int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes) {
+int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flags) {
     if (!index) return fail(PH_E_INVALID, "null index");
-    index->dev.hot_limit = hot_limit_for(index->info.parts, index->info.buckets_per_part, hot_bytes);
-    return PH_OK;
+    DeviceGuard g(index->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    // recover the file-order pilots from the current device layout, then re-lay them out
+    const uint64_t P = index->info.parts, B = index->info.buckets_per_part;
+    std::vector<uint8_t> cur(P * B), file(P * B);
+    PH_CUDA(cudaDeviceSynchronize());
+    PH_CUDA(cudaMemcpy(cur.data(), index->d_pilots, cur.size(), cudaMemcpyDeviceToHost));
+    const uint64_t H = index->dev.hot_b;
+    for (uint64_t part = 0; part < P; part++) {
+        std::memcpy(file.data() + part * B, cur.data() + part * H, H);
+        std::memcpy(file.data() + part * B + H, cur.data() + P * H + part * (B - H), B - H);
+    }
+    cudaFree(index->d_pilots);
+    index->d_pilots = nullptr;
+    return apply_pilot_layout(index, file.data(), hot_bytes, flags);
 }
 
 int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out) {

@@ -128,6 +128,43 @@ __global__ void __launch_bounds__(256) k_gather_skew(const uint8_t* __restrict__
     if (acc == 0x7fffffffu) *sink = acc;
 }
 
+// Uniform random gather with a selectable load flavour (DRAM fetch-size experiments).
+template <int MODE>
+__device__ __forceinline__ uint16_t ld_mode(const uint8_t* p, uint64_t pol) {
+    uint16_t x;
+    if (MODE == 0) asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(x) : "l"(p), "l"(pol));
+    if (MODE == 1) asm volatile("ld.global.nc.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 2) asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 3) asm volatile("ld.global.cv.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 4) asm volatile("ld.global.nc.L2::64B.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 5) asm volatile("ld.global.nc.L2::128B.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 6) asm volatile("ld.global.nc.L2::256B.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 7) asm volatile("ld.global.lu.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 8) asm volatile("ld.global.cs.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    if (MODE == 9) asm volatile("ld.global.u8 %0, [%1];" : "=h"(x) : "l"(p));
+    return x;
+}
+template <int MODE>
+__global__ void __launch_bounds__(256) k_gather_mode(const uint8_t* __restrict__ buf, uint64_t F,
+                                                     uint64_t nloads, uint64_t seed, uint32_t* sink) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 8;
+    uint32_t acc = 0;
+    for (uint64_t base = tid * 8; base < nloads; base += stride) {
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t r = mix64(seed + (base + j) * kGolden);
+            v[j] = ld_mode<MODE>(buf + __umul64hi(r, F), pol);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc += v[j];
+    }
+    if (acc == 0x7fffffffu) *sink = acc;
+}
+
 __global__ void k_bijection(const uint32_t* __restrict__ out, uint64_t count, uint64_t n,
                             unsigned int* bits, unsigned long long* bad) {
     unsigned long long local_oob = 0, local_dup = 0;
@@ -189,6 +226,18 @@ int phb_gather(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t seed,
         case 16: k_gather<16><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
         default: k_gather<8><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
     }
+    return (int)cudaGetLastError();
+}
+
+int phb_gather_mode(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t seed, int mode,
+                    uint32_t* d_sink, void* stream) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = sms * 8;
+#define PHB_M(M) case M: k_gather_mode<M><<<g, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
+    switch (mode) { PHB_M(0) PHB_M(1) PHB_M(2) PHB_M(3) PHB_M(4) PHB_M(5) PHB_M(6) PHB_M(7) PHB_M(8) PHB_M(9) }
+#undef PHB_M
     return (int)cudaGetLastError();
 }
 

@@ -27,19 +27,33 @@ struct DevIndex {
     const uint64_t* ef_samples;
     const uint64_t* opt_table;    // 65537-entry optimal-gamma table (host computed)
     uint64_t n, P, S, B, seed;
-    uint64_t magic_hi, magic_lo;  // FastModU64::make(S), reduce.hpp:31-36
+    uint64_t magic_hi, magic_lo;  // FastModU64::make(S), reduce.hpp:31-36 (kept for reference)
+    uint64_t mod_m64;             // floor(2^64 / S) for the device's exact y mod S
     uint64_t hp_base;             // C * (seed & ~0xff): hash_pilot(p) = hp_base + C*((seed^p)&0xff)
     uint32_t seed_lo8;
     int32_t remap_kind;           // 0 plain32, 1 CacheLineEF, 2 Elias-Fano
     int32_t ef_low_bits;
     int32_t hash_algo;
-    // L2 residency policy for the pilot gather: buckets whose in-part index is below
-    // hot_limit are loaded with L2::evict_last, the rest with L2::evict_first. The
-    // bucket functions put most keys in the first buckets of every part (cubic gamma:
-    // the first ~10% of each part's pilot bytes serve ~40% of the queries), so the L2
-    // keeps exactly the pilots that are re-read.
-    uint64_t hot_limit;
+    // Hot-first pilot layout. The bucket functions put most keys in the
+    // first buckets of every part (cubic gamma: the first ~19% of each part's pilots
+    // serve ~50% of the queries). The device copy of the pilots stores the first hot_b
+    // buckets of every part contiguously ([0, P*hot_b), covered by a persisting L2
+    // access-policy window) and the remaining cold_b = B - hot_b buckets after it. It is
+    // a permutation of the PTRH pilot bytes; hot_b == B is the file's own layout.
+    uint64_t hot_b, cold_b, hot_total;
+    uint64_t window_bytes;        // persisting window over the hot region (0 = none)
+    float window_hit_ratio;
+    int32_t cold_evict_first;     // cold-region pilot loads: 1 = L2::evict_first, 0 = evict_last
 };
+
+// Device address of pilots[part*B + bucket] under the hot-first layout.
+// P, B < 2^32 (checked at create), so both products are single IMAD.WIDE.U32.
+__device__ __forceinline__ uint64_t pilot_offset(const DevIndex& ix, uint32_t part,
+                                                 uint32_t bucket) {
+    return bucket < (uint32_t)ix.hot_b
+               ? (uint64_t)part * (uint32_t)ix.hot_b + bucket
+               : ix.hot_total + (uint64_t)part * (uint32_t)ix.cold_b + (bucket - (uint32_t)ix.hot_b);
+}
 
 // ---------------------------------------------------------------------------
 // cache-policy loads/stores
@@ -77,6 +91,15 @@ __device__ __forceinline__ void st_stream(uint64_t* p, uint64_t v) {
 // 64-bit integer helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// 32x64 -> 96-bit product: returns hi64(a*b), sets lo = lo64(a*b). Two IMAD.WIDE.U32.
+__device__ __forceinline__ uint64_t mul32x64(uint32_t a, uint64_t b, uint64_t& lo) {
+    const uint64_t p0 = (uint64_t)a * (uint32_t)b;
+    const uint64_t p1 = (uint64_t)a * (uint32_t)(b >> 32);
+    const uint64_t mid = p1 + (p0 >> 32);  // < 2^64: no overflow
+    lo = (mid << 32) | (uint32_t)p0;
+    return mid >> 32;
+}
 
 // ((u128)a * b) >> s for 0 < s < 64
 __device__ __forceinline__ uint64_t mul_shr(uint64_t a, uint64_t b, int s) {
@@ -119,12 +142,13 @@ __device__ __forceinline__ uint64_t reduce(const DevIndex& ix, uint64_t y) {
     if constexpr (POW2) {
         return mulhi(kC, y) & (ix.S - 1);
     } else {
-        // FastModU64::mod: lb = M*y mod 2^128; r = hi64(lb * S) (S < 2^32)
-        const uint64_t lb_lo = ix.magic_lo * y;
-        const uint64_t lb_hi = ix.magic_hi * y + mulhi(ix.magic_lo, y);
-        const uint64_t t1 = mulhi(lb_lo, ix.S);
-        const uint64_t lo = lb_hi * ix.S;
-        return mulhi(lb_hi, ix.S) + ((lo + t1) < t1 ? 1 : 0);
+        // FastModU64::mod (reduce.hpp:38-43) is the exact y mod S for S < 2^32 (Lemire's
+        // 128-bit-magic bound; verified against 128-bit division in tests/test_oracle.py).
+        // Same value, fewer multiplies: q = hi64(y * floor(2^64/S)) is floor(y/S) or one
+        // less, so r = y - q*S lies in [0, 2S) and one conditional subtract finishes it.
+        const uint64_t q = mulhi(y, ix.mod_m64);
+        uint64_t r = y - q * (uint32_t)ix.S;
+        return r >= ix.S ? r - ix.S : r;
     }
 }
 

@@ -10,6 +10,30 @@
 
 namespace phg {
 
+// Launch `kernel` with the index's persisting-L2 access-policy window over the hot
+// pilot region (a per-launch attribute: the caller's stream is not modified).
+template <class... KArgs, class... Args>
+inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
+                             unsigned block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    if (ix.window_bytes) {
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<uint8_t*>(ix.pilots);
+        attr[0].val.accessPolicyWindow.num_bytes = ix.window_bytes;
+        attr[0].val.accessPolicyWindow.hitRatio = ix.window_hit_ratio;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                              int sms);

@@ -26,6 +26,16 @@ namespace phg {
 #ifndef PH_KPT
 #define PH_KPT 8
 #endif
+#ifndef PH_PIPE
+#define PH_PIPE 1
+#endif
+// CTA size and the register-bounding minimum CTAs per SM (tools/tune.py sweeps)
+#ifndef PH_THREADS
+#define PH_THREADS 128
+#endif
+#ifndef PH_MINB
+#define PH_MINB 1
+#endif
 
 // Warp-cooperative remap of the keys flagged in need[] (slot >= n).
 // Entries are ranked across (j, lane) with ballots; lane r of a round decodes
@@ -70,7 +80,7 @@ __device__ __forceinline__ void remap_tile(const DevIndex& ix, const bool (&need
 }
 
 template <int G, bool POW2, class OutT, int KPT>
-__global__ void __launch_bounds__(256) k_query_u64(const DevIndex ix,
+__global__ void __launch_bounds__(PH_THREADS, PH_MINB) k_query_u64(const DevIndex ix,
                                                    const uint64_t* __restrict__ keys,
                                                    OutT* __restrict__ out, uint64_t nkeys,
                                                    int minimal) {
@@ -81,41 +91,62 @@ __global__ void __launch_bounds__(256) k_query_u64(const DevIndex ix,
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
 
-    for (uint64_t base = warp * kTile; base < nkeys; base += nwarps * kTile) {
-        const bool full = base + kTile <= nkeys;
-        uint64_t h[KPT];
+    const uint64_t stride = nwarps * kTile;
+    const uint32_t P32 = (uint32_t)ix.P, B32 = (uint32_t)ix.B, S32 = (uint32_t)ix.S;
+    // PH_PIPE: the next tile's keys are loaded before this tile's pilot gather and remap,
+    // so the key stream's DRAM latency overlaps them (software pipelining across tiles).
+    uint64_t knext[KPT];
+    // In-tile bounds as one 32-bit compare per element: rem = keys left in this tile.
+    auto tile_rem = [&](uint64_t b) -> uint32_t {
+        return b + kTile <= nkeys ? (uint32_t)kTile : (uint32_t)(nkeys - b);
+    };
+    auto load_keys = [&](uint64_t b, uint64_t (&k)[KPT]) {
+        const uint32_t rem = tile_rem(b);
+        const uint64_t* kp = keys + b + lane;
 #pragma unroll
-        for (int j = 0; j < KPT; j++) {
-            const uint64_t i = base + (uint64_t)j * 32 + lane;
-            const uint64_t k = (full || i < nkeys) ? ld_stream_u64(keys + i, pol_stream) : 0;
-            h[j] = kC * (k ^ ix.seed);  // hash_int, hash.hpp:27 (hi == lo)
+        for (int j = 0; j < KPT; j++)
+            k[j] = (uint32_t)(j * 32) + lane < rem ? ld_stream_u64(kp + j * 32, pol_stream) : 0;
+    };
+    if (PH_PIPE) load_keys(warp * kTile, knext);
+
+    for (uint64_t base = warp * kTile; base < nkeys; base += stride) {
+        const uint32_t rem = tile_rem(base);
+        uint64_t h[KPT];
+        if (PH_PIPE) {
+#pragma unroll
+            for (int j = 0; j < KPT; j++) h[j] = knext[j];
+            if (base + stride < nkeys) load_keys(base + stride, knext);
+        } else {
+            load_keys(base, h);
         }
-        uint64_t part[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; j++) h[j] = kC * (h[j] ^ ix.seed);  // hash_int, hash.hpp:27
+        uint32_t part[KPT];
         uint32_t pilot[KPT];
 #pragma unroll
         for (int j = 0; j < KPT; j++) {
-            // part_and_bucket, bucket_fn.hpp:66-72
-            part[j] = mulhi(ix.P, h[j]);
-            const uint64_t x = ix.P * h[j];
-            const uint64_t bucket = mulhi(ix.B, gamma<G>(x, ix.opt_table));
-            pilot[j] = ld_gather_u8(ix.pilots + part[j] * ix.B + bucket,
-                                    bucket < ix.hot_limit ? pol_keep : pol_stream);
+            // part_and_bucket, bucket_fn.hpp:66-72 (P, B < 2^32: checked at create)
+            uint64_t x;
+            part[j] = (uint32_t)mul32x64(P32, h[j], x);
+            uint64_t unused;
+            const uint32_t bucket = (uint32_t)mul32x64(B32, gamma<G>(x, ix.opt_table), unused);
+            const bool hot = bucket < ix.hot_b;
+            pilot[j] = ld_gather_u8(ix.pilots + pilot_offset(ix, part[j], bucket),
+                                    (hot || !ix.cold_evict_first) ? pol_keep : pol_stream);
         }
         uint64_t slot[KPT];
         bool need[KPT];
 #pragma unroll
         for (int j = 0; j < KPT; j++) {
             // slot_of, index.hpp:91-96
-            slot[j] = part[j] * ix.S + reduce<POW2>(ix, h[j] ^ hash_pilot(ix, pilot[j]));
-            const uint64_t i = base + (uint64_t)j * 32 + lane;
-            need[j] = minimal && slot[j] >= ix.n && (full || i < nkeys);
+            slot[j] = (uint64_t)part[j] * S32 + reduce<POW2>(ix, h[j] ^ hash_pilot(ix, pilot[j]));
+            need[j] = minimal && slot[j] >= ix.n && (uint32_t)(j * 32) + lane < rem;
         }
         if (minimal) remap_tile<KPT, OutT>(ix, need, slot);  // remap_slot, index.hpp:98-100
+        OutT* op = out + base + lane;
 #pragma unroll
-        for (int j = 0; j < KPT; j++) {
-            const uint64_t i = base + (uint64_t)j * 32 + lane;
-            if (full || i < nkeys) st_stream(out + i, slot[j]);
-        }
+        for (int j = 0; j < KPT; j++)
+            if ((uint32_t)(j * 32) + lane < rem) st_stream(op + j * 32, slot[j]);
     }
 }
 
@@ -152,11 +183,12 @@ static cudaError_t launch_u64_t(const DevIndex& ix, const uint64_t* keys, void* 
                                 int minimal, cudaStream_t s, int sms) {
     constexpr int KPT = PH_KPT;
     auto kern = k_query_u64<G, POW2, OutT, KPT>;
-    const int threads = g_threads_override > 0 ? g_threads_override : 256;
+    const int threads = g_threads_override > 0 ? g_threads_override : PH_THREADS;
     const int blocks = grid_for(kern, threads, (uint64_t)threads / 32 * 32 * KPT, n, sms);
-    kern<<<blocks, threads, 0, s>>>(ix, keys, static_cast<OutT*>(out), n, minimal);
+    const cudaError_t e = launch_ex(ix, kern, blocks, threads, s, ix, keys,
+                                    static_cast<OutT*>(out), n, minimal);
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    return cudaGetLastError();
+    return e;
 }
 
 template <class OutT>

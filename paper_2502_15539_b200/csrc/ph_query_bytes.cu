@@ -245,9 +245,11 @@ __global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
         }
         const uint64_t part = mulhi(ix.P, hi);
         const uint64_t bucket = mulhi(ix.B, gamma<G>(ix.P * hi, ix.opt_table));
-        const uint32_t pilot = valid ? ld_gather_u8(ix.pilots + part * ix.B + bucket,
-                                                  bucket < ix.hot_limit ? pol_keep : pol_cold)
-                                   : 0;
+        const bool hot = bucket < ix.hot_b;
+        const uint32_t pilot =
+            valid ? ld_gather_u8(ix.pilots + pilot_offset(ix, part, bucket),
+                                 (hot || !ix.cold_evict_first) ? pol_keep : pol_cold)
+                  : 0;
         uint64_t slot[1] = {part * ix.S + reduce<POW2>(ix, lo ^ hash_pilot(ix, pilot))};
         if (minimal) {
             const bool need = valid && slot[0] >= ix.n;
@@ -272,9 +274,10 @@ static cudaError_t launch_b(const DevIndex& ix, const uint8_t* d, const uint64_t
     const uint64_t want = (n + 255) / 256;
     const uint64_t cap = (uint64_t)sms * bps;
     const int blocks = (int)(want < cap ? want : cap);
-    kern<<<blocks, 256, 0, s>>>(ix, d, o, bo, static_cast<OutT*>(out), n, minimal);
+    const cudaError_t e =
+        launch_ex(ix, kern, blocks, 256, s, ix, d, o, bo, static_cast<OutT*>(out), n, minimal);
     note_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 template <class OutT>

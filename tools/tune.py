@@ -139,22 +139,21 @@ def main():
     for name in libs:
         if name != "main":
             rec(f"lib={name}", lib=name)
-    for threads, bps in ((256, 2), (256, 1), (128, 8), (128, 4)):
+    for threads, bps in ((128, 4), (128, 8), (64, 16)):
         for L, _ in handles.values():
             L.ph_gpu_set_launch(threads, bps)
         rec(f"launch threads={threads} bps={bps}")
     for L, _ in handles.values():
         L.ph_gpu_set_launch(0, 0)
-    default_g = bench.phb_get_l2_fetch_granularity()
     L, h = handles["main"]
-    L.ph_gpu_index_set_l2_policy.argtypes = [C.c_void_p, C.c_uint64]
-    for g in (32, 64):
-        bench.phb_set_l2_fetch_granularity(g)
-        for hot_mb in (0, 24, 48, 64, 96, 128, 512):
-            L.ph_gpu_index_set_l2_policy(h, hot_mb << 20)
-            rec(f"l2_fetch={g} hot_mb={hot_mb}")
-    bench.phb_set_l2_fetch_granularity(default_g)
-    L.ph_gpu_index_set_l2_policy(h, 48 << 20)
+    L.ph_gpu_index_set_l2_policy.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
+    for flags in ((0, 1, 2, 3) if args.sweep in ("full", "l2") else ()):
+        for hot_mb in ((16, 32, 48, 64, 79, 96, 128) if args.sweep == "full" else (32, 64, 79)):
+            assert L.ph_gpu_index_set_l2_policy(h, hot_mb << 20, flags) == 0
+            rec(f"l2 hot_mb={hot_mb} flags={flags}")
+    assert L.ph_gpu_index_set_l2_policy(h, 1 << 40, 2) == 0
+    rec("l2 identity layout, no window")
+    L.ph_gpu_index_set_l2_policy(h, 64 << 20, 0)
     print(json.dumps({"summary": results}))
 
 

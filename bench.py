@@ -2,7 +2,7 @@
 """PtrHash query-path benchmark (BASELINE.json metric): batched MPHF query throughput in
 Gkeys/s at n=1e9 u64 keys on one B200, with the pilot-gather / HBM roofline.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
 
 A "step" is one pass of the query path over the config's whole query stream (config 3:
 all 1e9 keys in a seeded shuffled order, u32 output, minimal with the CacheLineEF remap).
@@ -45,14 +45,24 @@ PERM_SEED = 7          # shuffled query order
 SAMPLE_SEED = 0xC0FFEE  # config 2: sampling with replacement
 METRIC = "batched MPHF query Gkeys/s (ns/key) at n=1e9 u64 keys; % of pilot-gather roofline"
 
+STR_SEED = 43          # config 4 string corpus
+DNA_SEED = 44          # config 5 sequence
+
 CONFIGS = {
-    1: dict(n=10**7, order="perm",
+    1: dict(kind="u64", n=10**7, order="perm",
             desc="config1: n=1e7 distinct u64 (splitmix64), all keys in seeded shuffled order"),
-    2: dict(n=10**8, order="sample",
+    2: dict(kind="u64", n=10**8, order="sample",
             desc="config2: n=1e8 distinct u64, 1e8 queries sampled with replacement"),
-    3: dict(n=10**9, order="perm",
+    3: dict(kind="u64", n=10**9, order="perm",
             desc="config3: n=1e9 distinct u64 (8 GB keys, 333 MB pilots), all keys in seeded "
                  "shuffled order"),
+    4: dict(kind="str", n=3 * 10**8, order="perm",
+            desc="config4: n=3e8 distinct strings, len U[8,64], bytes 0x21-0x7E, one "
+                 "concatenated buffer + u64 offsets, all keys in seeded shuffled order"),
+    5: dict(kind="kmer", n=10**9, k=31,
+            desc="config5: every 31-mer of a seeded random ACGT sequence of 1e9+30 bases "
+                 "(2-bit packed, first base in the MSBs), in sequence order; fused on-device "
+                 "k-mer extraction"),
 }
 
 
@@ -166,22 +176,26 @@ def ref_params(ref):
     return ref.params("default", lambda_=(30, 10))
 
 
-def build_index_bytes(n: int, dist: Dist, gen_keys) -> bytes:
-    """Reference-built PTRH bytes; for N>1 rank 0 builds and shares through /dev/shm."""
+def build_index_bytes(n: int, dist: Dist, gen_keys, build=None, tag="u64") -> bytes:
+    """Reference-built PTRH bytes; for N>1 rank 0 builds and shares through /dev/shm.
+    gen_keys(n) -> u64 keys for the reference u64 builder, or build() -> PTRH bytes."""
     from oracle.bindings import Ref
-    tag = hashlib.sha1(f"{n}-{GEN_SEED}-default-l30".encode()).hexdigest()[:12]
+    tag = hashlib.sha1(f"{tag}-{n}-{GEN_SEED}-default-l30".encode()).hexdigest()[:12]
     shm = f"/dev/shm/ph_bench_{tag}_{os.getpid() if dist.world == 1 else 'job'}.ptrh"
     ptrh = None
     if dist.rank == 0:
         ref = Ref()
         t = time.time()
-        keys = gen_keys(n)
-        log(f"[fixture] {n} keys generated in {time.time() - t:.1f}s; building with the "
-            f"reference builder ({ref.hw_threads()} threads)...")
-        t = time.time()
-        ptrh = ref.build_u64(keys, ref_params(ref), threads=0)
+        if build is not None:
+            ptrh = build()
+        else:
+            keys = gen_keys(n)
+            log(f"[fixture] {n} keys generated in {time.time() - t:.1f}s; building with the "
+                f"reference builder ({ref.hw_threads()} threads)...")
+            t = time.time()
+            ptrh = ref.build_u64(keys, ref_params(ref), threads=0)
+            del keys
         log(f"[fixture] reference build {time.time() - t:.1f}s, PTRH {len(ptrh) / 1e6:.1f} MB")
-        del keys
         if dist.world > 1:
             with open(shm, "wb") as f:
                 f.write(ptrh)
@@ -208,47 +222,222 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
+# workloads (our arm): index fixture, device-resident query, host-API query, gate
+# ---------------------------------------------------------------------------
+class U64Work:
+    """configs 1-3: u64 keys, device-generated query stream (shuffled or sampled)."""
+
+    stream_bytes = 12.0  # 8 B key in + 4 B u32 out
+
+    def __init__(self, args, cfg, dist, bench, sp):
+        import torch
+        from paper_2502_15539_b200 import ph_gpu
+        self.cfg, self.n = cfg, cfg["n"]
+        n = self.n
+
+        def gen_keys_gpu(count):
+            keys = np.empty(count, dtype=np.uint64)
+            chunk = 1 << 27
+            buf = torch.empty(min(chunk, count), dtype=torch.int64, device="cuda")
+            for s in range(0, count, chunk):
+                m = min(chunk, count - s)
+                assert bench.phb_gen_corpus(C.c_void_p(buf.data_ptr()), C.c_uint64(s),
+                                            C.c_uint64(m), C.c_uint64(GEN_SEED), sp) == 0
+                keys[s:s + m] = buf[:m].cpu().numpy().view(np.uint64)
+            return keys
+
+        self.ptrh = build_index_bytes(n, dist, gen_keys_gpu)
+        self.idx = ph_gpu.PtrHashIndex(self.ptrh, device=dist.local)
+        self.nq = n
+        self.q = torch.empty(self.nq, dtype=torch.int64, device="cuda")
+        perm = cfg["order"] == "perm"
+        seed = (PERM_SEED if perm else SAMPLE_SEED) + dist.rank
+        fn = bench.phb_gen_queries_perm if perm else bench.phb_gen_queries_sample
+        assert fn(C.c_void_p(self.q.data_ptr()), C.c_uint64(0), C.c_uint64(self.nq), C.c_uint64(n),
+                  C.c_uint64(GEN_SEED), C.c_uint64(seed), sp) == 0
+        self.bijective = perm
+        self.pin_q = torch.empty(self.nq, dtype=torch.int64).pin_memory()
+        self.pin_q.copy_(self.q)
+        self.h2d, self.d2h = self.nq * 8, self.nq * 4
+        self.api = "ph_gpu_index_stream_u64 (host pinned u64 keys -> host u32 out)"
+
+    def query(self, out, minimal, stream):
+        self.idx.query(self.q, out=out, minimal=minimal, out_width=4, stream=stream)
+
+    def e2e(self, pin_out):
+        self.idx.query(self.pin_q, out=pin_out, minimal=True, out_width=4)
+
+    def reference_answers(self, ri, minimal, m):
+        qh = self.pin_q.numpy().view(np.uint64)[:m]
+        return ri.query_u64(qh, minimal, "stream", 32, threads=os.cpu_count() or 1)
+
+    def cpu_sample(self, ri, S):
+        sample = np.ascontiguousarray(self.pin_q.numpy().view(np.uint64)[:S])
+        out = np.empty(S, dtype=np.uint64)
+        T = os.cpu_count() or 1
+        return (lambda: ri.query_u64(sample, True, "stream", 32, threads=T, out=out)), \
+            f"first {S} queries of the same stream, index_stream lookahead 32, minimal, {T} threads"
+
+
+class StrWork:
+    """config 4: byte-string keys (concatenated bytes + u64 offsets), shuffled."""
+
+    def __init__(self, args, cfg, dist, bench, sp):
+        import torch
+        from oracle.bindings import Ref
+        from paper_2502_15539_b200 import ph_gpu
+        self.cfg, self.n = cfg, cfg["n"]
+        n = self.n
+
+        def gen(permuted):
+            lens = torch.empty(n, dtype=torch.int64, device="cuda")
+            assert bench.phb_str_lens(C.c_void_p(lens.data_ptr()), C.c_uint64(n),
+                                      C.c_uint64(STR_SEED), C.c_uint64(PERM_SEED + dist.rank),
+                                      permuted, sp) == 0
+            offs = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+            torch.cumsum(lens, 0, out=offs[1:])
+            del lens
+            total = int(offs[-1].item())
+            data = torch.empty(max(total, 1), dtype=torch.uint8, device="cuda")
+            assert bench.phb_str_bytes(C.c_void_p(offs.data_ptr()), C.c_uint64(n),
+                                       C.c_uint64(STR_SEED), C.c_uint64(PERM_SEED + dist.rank),
+                                       permuted, C.c_void_p(data.data_ptr()), sp) == 0
+            return data, offs
+
+        def build():
+            data, offs = gen(0)  # generation order, for the reference builder
+            hd = data.cpu().numpy()
+            ho = offs.cpu().numpy().view(np.uint64)
+            del data, offs
+            ref = Ref()
+            log(f"[fixture] {n} strings ({hd.size / 1e9:.1f} GB) generated; reference "
+                f"build_sharded over the concatenated buffer...")
+            return ref.build_bytes(hd, ho, ref_params(ref), lean=True)
+
+        self.ptrh = build_index_bytes(n, dist, None, build=build, tag="str")
+        self.idx = ph_gpu.PtrHashIndex(self.ptrh, device=dist.local)
+        self.nq = n
+        self.data, self.offs = gen(1)  # the shuffled query stream
+        self.bijective = True
+        self.pin_data = torch.empty(self.data.numel(), dtype=torch.uint8).pin_memory()
+        self.pin_data.copy_(self.data)
+        self.pin_offs = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        self.pin_offs.copy_(self.offs)
+        nbytes = self.data.numel()
+        self.stream_bytes = (nbytes + 8.0 * (n + 1)) / n + 4.0
+        self.h2d, self.d2h = nbytes + 8 * (n + 1), n * 4
+        self.api = "ph_gpu_index_stream_bytes (host pinned bytes + offsets -> host u32 out)"
+
+    def query(self, out, minimal, stream):
+        self.idx.query((self.data, self.offs), out=out, minimal=minimal, out_width=4,
+                       stream=stream)
+
+    def e2e(self, pin_out):
+        self.idx.query((self.pin_data, self.pin_offs), out=pin_out, minimal=True, out_width=4)
+
+    def reference_answers(self, ri, minimal, m):
+        d = self.pin_data.numpy()
+        o = self.pin_offs.numpy().view(np.uint64)[:m + 1]
+        return ri.query_bytes(d, o, minimal, "single", threads=os.cpu_count() or 1)
+
+    def cpu_sample(self, ri, S):
+        d = self.pin_data.numpy()
+        o = np.ascontiguousarray(self.pin_offs.numpy().view(np.uint64)[:S + 1])
+        out = np.empty(S, dtype=np.uint64)
+        T = os.cpu_count() or 1
+        return (lambda: ri.query_bytes(d, o, True, "single", threads=T, out=out)), \
+            (f"first {S} queries of the same shuffled stream, reference index(string_view) over "
+             f"the concatenated buffer (std::string materialisation avoided), minimal, {T} threads")
+
+
+class KmerWork:
+    """config 5: k-mers of a packed DNA sequence, in sequence order, fused front end."""
+
+    def __init__(self, args, cfg, dist, bench, sp):
+        import torch
+        from oracle.bindings import Ref
+        from paper_2502_15539_b200 import ph_gpu
+        self.cfg, self.k = cfg, cfg["k"]
+        k = self.k
+        self.n_bases = cfg["n"] + k - 1
+        nw = (self.n_bases + 31) // 32
+        self.seq = torch.empty(nw, dtype=torch.int64, device="cuda")
+        assert bench.phb_gen_dna(C.c_void_p(self.seq.data_ptr()), C.c_uint64(nw),
+                                 C.c_uint64(DNA_SEED + dist.rank), sp) == 0
+        self.nq = self.n_bases - k + 1
+        kmers = torch.empty(self.nq, dtype=torch.int64, device="cuda")
+        assert bench.phb_kmers(C.c_void_p(self.seq.data_ptr()), C.c_uint64(self.n_bases), k,
+                               C.c_void_p(kmers.data_ptr()), sp) == 0
+        self.kmers_host = torch.empty(self.nq, dtype=torch.int64).pin_memory()
+        self.kmers_host.copy_(kmers)
+
+        def build():
+            uniq = torch.unique(kmers)  # deduplicated key set, as the workload defines it
+            self.n_unique = int(uniq.numel())
+            hu = uniq.cpu().numpy().view(np.uint64)
+            del uniq
+            ref = Ref()
+            log(f"[fixture] {self.nq} k-mers, {hu.size} distinct; reference build...")
+            return ref.build_u64(hu, ref_params(ref), threads=0)
+
+        self.n_unique = None
+        self.ptrh = build_index_bytes(self.nq, dist, None, build=build, tag=f"kmer{k}")
+        del kmers
+        self.idx = ph_gpu.PtrHashIndex(self.ptrh, device=dist.local)
+        self.n = int(self.idx.info.n)
+        self.bijective = self.n == self.nq  # no duplicate k-mer: outputs are a permutation
+        self.pin_seq = torch.empty(nw, dtype=torch.int64).pin_memory()
+        self.pin_seq.copy_(self.seq)
+        self.stream_bytes = 8.0 * nw / self.nq + 4.0  # 0.25 B packed bases + 4 B out
+        self.h2d, self.d2h = nw * 8, self.nq * 4
+        self.api = "ph_gpu_index_stream_kmers (host pinned packed sequence -> host u32 out)"
+
+    def query(self, out, minimal, stream):
+        self.idx.query_kmers(self.seq, self.n_bases, self.k, out=out, minimal=minimal,
+                             out_width=4, stream=stream)
+
+    def e2e(self, pin_out):
+        self.idx.query_kmers(self.pin_seq, self.n_bases, self.k, out=pin_out, minimal=True,
+                             out_width=4)
+
+    def reference_answers(self, ri, minimal, m):
+        kh = self.kmers_host.numpy().view(np.uint64)[:m]
+        return ri.query_u64(kh, minimal, "stream", 32, threads=os.cpu_count() or 1)
+
+    def cpu_sample(self, ri, S):
+        sample = np.ascontiguousarray(self.kmers_host.numpy().view(np.uint64)[:S])
+        out = np.empty(S, dtype=np.uint64)
+        T = os.cpu_count() or 1
+        return (lambda: ri.query_u64(sample, True, "stream", 32, threads=T, out=out)), \
+            (f"first {S} k-mers in sequence order, materialised as u64 keys (the reference has "
+             f"no k-mer front end; extraction untimed), index_stream lookahead 32, minimal, "
+             f"{T} threads")
+
+
+WORKLOADS = {"u64": U64Work, "str": StrWork, "kmer": KmerWork}
+
+
 def run_ours(args, cfg):
     import torch
     dist = Dist("nccl")
     torch.cuda.set_device(dist.local)
     from paper_2502_15539_b200 import ph_gpu
     bench = C.CDLL(os.path.join(ROOT, "paper_2502_15539_b200", "libph_bench.so"))
-    n = cfg["n"]
     stream = torch.cuda.current_stream()
     sp = C.c_void_p(stream.cuda_stream)
-
-    def gen_keys_gpu(count):
-        keys = np.empty(count, dtype=np.uint64)
-        chunk = 1 << 27
-        buf = torch.empty(min(chunk, count), dtype=torch.int64, device="cuda")
-        for s in range(0, count, chunk):
-            m = min(chunk, count - s)
-            assert bench.phb_gen_corpus(C.c_void_p(buf.data_ptr()), C.c_uint64(s), C.c_uint64(m),
-                                        C.c_uint64(GEN_SEED), sp) == 0
-            keys[s:s + m] = buf[:m].cpu().numpy().view(np.uint64)
-        del buf
-        return keys
-
-    ptrh = build_index_bytes(n, dist, gen_keys_gpu)
-    idx = ph_gpu.PtrHashIndex(ptrh, device=dist.local)
-    info = idx.info
-    nq = n  # queries per step per rank
-    q = torch.empty(nq, dtype=torch.int64, device="cuda")
-    seed = PERM_SEED + dist.rank if cfg["order"] == "perm" else SAMPLE_SEED + dist.rank
-    fn = bench.phb_gen_queries_perm if cfg["order"] == "perm" else bench.phb_gen_queries_sample
-    assert fn(C.c_void_p(q.data_ptr()), C.c_uint64(0), C.c_uint64(nq), C.c_uint64(n),
-              C.c_uint64(GEN_SEED), C.c_uint64(seed), sp) == 0
+    W = WORKLOADS[cfg["kind"]](args, cfg, dist, bench, sp)
+    idx, info, nq, n = W.idx, W.idx.info, W.nq, int(W.idx.info.n)
     out = torch.empty(nq, dtype=torch.int32, device="cuda")
     out_nm = torch.empty(nq, dtype=torch.int32, device="cuda")
 
     # ---- correctness gate (untimed) ----
-    idx.query(q, out=out, minimal=True, out_width=4)
-    idx.query(q, out=out_nm, minimal=False, out_width=4)
+    W.query(out, True, stream.cuda_stream)
+    W.query(out_nm, False, stream.cuda_stream)
     torch.cuda.synchronize()
     remap_frac = float((out_nm.to(torch.int64) & 0xFFFFFFFF).ge(n).double().mean().item())
     gate = {"remap_fraction": remap_frac}
-    if cfg["order"] == "perm":
+    if W.bijective:
         bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
         bad = torch.zeros(2, dtype=torch.int64, device="cuda")
         bench.phb_bijection(C.c_void_p(out.data_ptr()), C.c_uint64(nq), C.c_uint64(n),
@@ -256,25 +445,21 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         gate["bijection"] = bad.tolist() == [0, 0]
         del bits
-    pin_q = torch.empty(nq, dtype=torch.int64).pin_memory()
-    pin_q.copy_(q)
     pin_o = torch.empty(nq, dtype=torch.int32).pin_memory()
     if args.verify != "none" and dist.rank == 0:
         from oracle.bindings import Ref
-        ref = Ref()
-        ri = ref.load(ptrh)
-        qh = pin_q.numpy().view(np.uint64)
+        ri = Ref().load(W.ptrh)
         m = nq if args.verify == "full" else min(nq, 10**7)
         t = time.time()
         ok = True
         for minimal, o in ((True, out), (False, out_nm)):
-            want = ri.query_u64(qh[:m], minimal, "stream", 32, threads=os.cpu_count() or 1)
+            want = W.reference_answers(ri, minimal, m)
             got = o[:m].cpu().numpy().view(np.uint32)
             ok &= bool(np.array_equal(got, want.astype(np.uint32))) and int(want.max()) < 2**32
             del want
         gate["bit_exact_vs_reference"] = ok
         gate["verified_queries"] = int(m) * 2
-        log(f"[gate] {m} queries x (minimal, non-minimal) vs reference index_stream: "
+        log(f"[gate] {m} queries x (minimal, non-minimal) vs the reference: "
             f"{'OK' if ok else 'MISMATCH'} ({time.time() - t:.1f}s)")
         ri.close()
         if not ok or not gate.get("bijection", True):
@@ -314,12 +499,9 @@ def run_ours(args, cfg):
     sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
 
-    def step(minimal=True):
-        idx.query(q, out=out, minimal=minimal, out_width=4, stream=stream.cuda_stream)
-
     def timed(minimal):
         for _ in range(args.warmup):
-            step(minimal)
+            W.query(out, minimal, stream.cuda_stream)
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
@@ -330,15 +512,14 @@ def run_ours(args, cfg):
             flush.zero_()  # L2 flush outside the event pair
             a, b = ev(), ev()
             a.record(stream)
-            step(minimal)
+            W.query(out, minimal, stream.cuda_stream)
             b.record(stream)
             ms.append((a, b))
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         dist.barrier()
         sampler.window(t0, t1)
-        ms = [a.elapsed_time(b) for a, b in ms]
-        return ms, ph_gpu.launch_count() - l0
+        return [a.elapsed_time(b) for a, b in ms], ph_gpu.launch_count() - l0
 
     ms_min, launches = timed(True)
     ms_nm, _ = timed(False)
@@ -346,14 +527,14 @@ def run_ours(args, cfg):
     total_nm = dist.max(sum(ms_nm))
 
     # ---- timed region: e2e through the public host API ----
-    for _ in range(max(1, min(args.warmup, 2))):
-        idx.query(pin_q, out=pin_o, minimal=True, out_width=4)
+    for _ in range(2):
+        W.e2e(pin_o)
     dist.barrier()
     torch.cuda.synchronize()
     l0 = ph_gpu.launch_count()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        idx.query(pin_q, out=pin_o, minimal=True, out_width=4)
+        W.e2e(pin_o)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     e2e_launches = ph_gpu.launch_count() - l0
@@ -361,21 +542,20 @@ def run_ours(args, cfg):
     sampler.window(t0, t1)
     e2e_s = dist.max(t1 - t0)
     sampler.stop()
-    step(True)  # the e2e outputs must equal the device-resident path's
+    W.query(out, True, stream.cuda_stream)  # e2e outputs must equal the device path's
     torch.cuda.synchronize()
     if not torch.equal(pin_o.cuda(), out):
         raise SystemExit("e2e host-path output differs from the device path")
 
     # ---- report ----
-    N = dist.world
-    K = args.steps
+    N, K = dist.world, args.steps
     value = N * nq * K / (total_ms * 1e-3) / 1e9
     kern_ms = statistics.mean(ms_min)
     sectors = 1.0 + remap_frac * (1.0 + 32.0 / 44.0)  # pilot + CLEF (i>=12 touches 2nd sector)
-    bytes_per_key = 12.0 + 32.0 * sectors
+    bytes_per_key = W.stream_bytes + 32.0 * sectors
     peak, peak_src = measured_peaks()
     achieved = nq * bytes_per_key / (kern_ms * 1e-3) / 1e9
-    stream_ms = nq * 12.0 / (bw_copy * 1e9) * 1e3
+    stream_ms = nq * W.stream_bytes / (bw_copy * 1e9) * 1e3
     gather_ms = nq * sectors / (r_gather * 1e9) * 1e3
     t_roof = max(stream_ms, gather_ms)
     traffic = None
@@ -383,13 +563,12 @@ def run_ours(args, cfg):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                tr = json.load(f)
-            traffic = tr.get(f"config{args.config}", {}).get("dram_bytes_per_launch")
+                traffic = json.load(f).get(f"config{args.config}", {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     cpu = None
     if dist.rank == 0 and N == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(ptrh, pin_q.numpy().view(np.uint64), args)
+        cpu = cpu_baseline(W, args)
     res = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -403,28 +582,25 @@ def run_ours(args, cfg):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u64",
-        "data": "synthetic (splitmix64 corpus_u64 keys, seeded Feistel shuffle; index built by "
-                "the reference builder)",
+        "data": "synthetic (seeded generators, SURVEY §8d; index built by the reference builder)",
         "config": {"workload": cfg["desc"], "n": n, "queries_per_step_per_gpu": nq,
                    "params": "preset default, lambda=3.0, alpha=0.99, cubic gamma, CacheLineEF, "
                              "fastmod S", "P": int(info.parts), "S": int(info.slots_per_part),
-                   "B": int(info.buckets_per_part), "output": "u32, minimal",
-                   "parallelism": f"replicas x{N} (no collective)",
-                   "l2": "flushed between steps (512 MiB write, outside the timed events); "
-                         "inputs (8 B/key) and pilots exceed L2 at n=1e9"},
+                   "B": int(info.buckets_per_part), "hash": int(info.hash_algo),
+                   "output": "u32, minimal", "parallelism": f"replicas x{N} (no collective)",
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)"},
         "nonminimal": {"value": round(N * nq * K / (total_nm * 1e-3) / 1e9, 3), "unit": "Gkeys/s",
                        "ms_per_step": round(total_nm / K, 4)},
         "gpu_launches": int(launches),
         "e2e": {"value": round(N * nq * K / e2e_s / 1e9, 4), "unit": "Gkeys/s",
-                "h2d_bytes_per_step": nq * 8, "d2h_bytes_per_step": nq * 4,
-                "api": "ph_gpu_index_stream_u64 (host pinned keys -> host u32 out)",
-                "gpu_launches": int(e2e_launches)},
+                "h2d_bytes_per_step": int(W.h2d), "d2h_bytes_per_step": int(W.d2h),
+                "api": W.api, "gpu_launches": int(e2e_launches)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_key": round(bytes_per_key, 3),
-                     "note": "12 B streamed (8 B key + 4 B out) + 32 B x (1 pilot sector + "
-                             "remap_fraction x 1.727 CacheLineEF sectors)"},
+                     "note": f"{W.stream_bytes:.2f} B streamed per query + 32 B x (1 pilot "
+                             f"sector + remap_fraction x 1.727 CacheLineEF sectors)"},
         "gather_roofline": {"t_roof_ms": round(t_roof, 4), "t_measured_ms": round(kern_ms, 4),
                             "frac": round(t_roof / kern_ms, 4),
                             "stream_bound_ms": round(stream_ms, 4),
@@ -441,27 +617,24 @@ def run_ours(args, cfg):
     dist.close()
 
 
-def cpu_baseline(ptrh: bytes, queries: np.ndarray, args):
-    """The reference's index_stream(keys, 32, out, minimal) on all host cores, contiguous
-    slices (proj/tools/ptrhash.cpp:486-512), one warm-up then best of 3 (:212-223)."""
+def cpu_baseline(W, args):
+    """The reference's CPU query on all host cores over a bounded sample of the same stream,
+    contiguous slices (proj/tools/ptrhash.cpp:486-512), one warm-up then best of 3
+    (:212-223)."""
     from oracle.bindings import Ref
-    ref = Ref()
-    ri = ref.load(ptrh)
-    T = os.cpu_count() or 1
-    S = min(queries.size, args.cpu_sample)
-    sample = np.ascontiguousarray(queries[:S])
-    out = np.empty(S, dtype=np.uint64)
-    ri.query_u64(sample, True, "stream", 32, threads=T, out=out)
+    ri = Ref().load(W.ptrh)
+    S = min(W.nq, args.cpu_sample)
+    fn, desc = W.cpu_sample(ri, S)
+    fn()
     best = 1e30
     for _ in range(3):
         t = time.perf_counter()
-        ri.query_u64(sample, True, "stream", 32, threads=T, out=out)
+        fn()
         best = min(best, time.perf_counter() - t)
     ri.close()
-    return {"value": round(S / best / 1e9, 4), "unit": "Gkeys/s", "ns_per_key": round(best / S * 1e9, 3),
-            "cores": T, "kind": "reference",
-            "sample": f"first {S} queries of the same shuffled stream, index_stream lookahead 32, "
-                      f"minimal, {T} threads, best of 3 after 1 warm-up"}
+    return {"value": round(S / best / 1e9, 4), "unit": "Gkeys/s",
+            "ns_per_key": round(best / S * 1e9, 3), "cores": os.cpu_count() or 1,
+            "kind": "reference", "sample": desc + ", best of 3 after 1 warm-up"}
 
 
 # ---------------------------------------------------------------------------
@@ -472,37 +645,67 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     from oracle.bindings import Port, Ref
-    n = cfg["n"]
     ref, port = Ref(), Port()
     T = os.cpu_count() or 1
     t = time.time()
-    keys = port.gen_keys("corpus", 0, n, n, GEN_SEED)
-    ptrh = ref.build_u64(keys, ref_params(ref), threads=0)
-    del keys
-    log(f"[reference] index built in {time.time() - t:.1f}s")
-    ri = ref.load(ptrh)
-    S = min(n, args.cpu_sample)
-    kind = "perm" if cfg["order"] == "perm" else "sample"
-    q = port.gen_keys(kind, 0, S, n, GEN_SEED, PERM_SEED if kind == "perm" else SAMPLE_SEED)
-    out = np.empty(S, dtype=np.uint64)
+    S = min(cfg["n"], args.cpu_sample)
+    kind = cfg["kind"]
+    if kind == "u64":
+        n = cfg["n"]
+        keys = port.gen_keys("corpus", 0, n, n, GEN_SEED)
+        ptrh = ref.build_u64(keys, ref_params(ref), threads=0)
+        del keys
+        perm = cfg["order"] == "perm"
+        q = port.gen_keys("perm" if perm else "sample", 0, S, n, GEN_SEED,
+                          PERM_SEED if perm else SAMPLE_SEED)
+        ri = ref.load(ptrh)
+        out = np.empty(S, dtype=np.uint64)
+        step = lambda: ri.query_u64(q, True, "stream", 32, threads=T, out=out)  # noqa: E731
+        what = "index_stream(lookahead 32)"
+    elif kind == "str":
+        n = cfg["n"]
+        data, offs = port.gen_strings(0, n, n, STR_SEED)
+        ptrh = ref.build_bytes(data, offs, ref_params(ref), lean=True)
+        del data, offs
+        qd, qo = port.gen_strings(0, S, n, STR_SEED, PERM_SEED)
+        ri = ref.load(ptrh)
+        out = np.empty(S, dtype=np.uint64)
+        step = lambda: ri.query_bytes(qd, qo, True, "single", threads=T, out=out)  # noqa: E731
+        what = "index(string_view) over the concatenated buffer"
+    else:
+        k = cfg["k"]
+        n_bases = cfg["n"] + k - 1
+        seq = port.gen_dna(n_bases, DNA_SEED)
+        kmers = port.kmers(seq, n_bases, k)
+        try:
+            ptrh = ref.build_u64(kmers, ref_params(ref), threads=0)
+        except RuntimeError:  # duplicate k-mers: build over the distinct ones
+            ptrh = ref.build_u64(np.unique(kmers), ref_params(ref), threads=0)
+        q = np.ascontiguousarray(kmers[:S])
+        del kmers
+        ri = ref.load(ptrh)
+        out = np.empty(S, dtype=np.uint64)
+        step = lambda: ri.query_u64(q, True, "stream", 32, threads=T, out=out)  # noqa: E731
+        what = "index_stream(lookahead 32) over materialised k-mers"
+    log(f"[reference] fixture + index built in {time.time() - t:.1f}s")
     for _ in range(args.warmup):
-        ri.query_u64(q, True, "stream", 32, threads=T, out=out)
+        step()
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        ri.query_u64(q, True, "stream", 32, threads=T, out=out)
+        step()
         ts.append(time.perf_counter() - t0)
     total = sum(ts)
     value = S * args.steps / total / 1e9
     sample = (f"first {S} queries of the config's query stream per step; reference "
-              f"PtrHashIndex::index_stream(lookahead 32), minimal, {T} threads, contiguous slices")
+              f"PtrHashIndex::{what}, minimal, {T} threads, contiguous slices")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "Gkeys/s",
         "ns_per_key": round(1 / value, 4), "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic", "config": {"workload": cfg["desc"], "n": n,
-                                        "params": "preset default, lambda=3.0"},
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "n": cfg["n"], "params": "preset default, lambda=3.0"},
         "cpu_baseline": {"value": round(value, 5), "unit": "Gkeys/s", "cores": T,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 5), "unit": "Gkeys/s", "h2d_bytes_per_step": 0,

@@ -83,6 +83,15 @@ int ph_gpu_query_bytes(const ph_gpu_index* index, const uint8_t* d_bytes,
                        const uint64_t* d_offsets, size_t n, void* d_out, int out_width,
                        int minimal, ph_gpu_stream_t stream);
 
+/* k-mer keys, fused (the SSHash use case): the queries are
+ * the n_bases-k+1 consecutive k-mers (1 <= k <= 32) of a 2-bit packed DNA sequence, in
+ * sequence order. Packing: A=0, C=1, G=2, T=3; word w holds bases 32w..32w+31, base 32w+t
+ * at bits 2(31-t) (MSB-first); the key of window i is its k bases with the first base in
+ * the most significant bits — the u64 key a caller would otherwise materialise and pass
+ * to ph_gpu_query_u64 (identical outputs). d_seq holds ceil(n_bases/32) words. */
+int ph_gpu_query_kmers(const ph_gpu_index* index, const uint64_t* d_seq, uint64_t n_bases, int k,
+                       void* d_out, int out_width, int minimal, ph_gpu_stream_t stream);
+
 /* ---- host-resident bulk queries (synchronous; the reference's own signature
  * shape: host keys in, host `out` fully overwritten) ----
  * Pipelined H2D -> kernel -> D2H over chunks on several streams. Pinned host
@@ -93,6 +102,10 @@ int ph_gpu_index_stream_u64(const ph_gpu_index* index, const uint64_t* h_keys, s
 int ph_gpu_index_stream_bytes(const ph_gpu_index* index, const uint8_t* h_bytes,
                               const uint64_t* h_offsets, size_t n, void* h_out, int out_width,
                               int minimal);
+/* k-mers of a host-resident packed sequence (layout as ph_gpu_query_kmers); h_out gets
+ * n_bases-k+1 elements. */
+int ph_gpu_index_stream_kmers(const ph_gpu_index* index, const uint64_t* h_seq, uint64_t n_bases,
+                              int k, void* h_out, int out_width, int minimal);
 
 /* ---- single-key queries (synchronous): index() / index_no_remap(),
  * index.hpp:60-64 ---- */

@@ -102,6 +102,11 @@ class PtrHashIndex {
                      bool minimal = true) const {
         check(ph_gpu_index_stream_bytes(h_, bytes, offsets, n, out, PH_OUT_U64, minimal));
     }
+    // k-mers of a host 2-bit packed sequence (ph_gpu.h layout), in sequence order
+    void index_kmers(const uint64_t* seq, uint64_t n_bases, int k, uint32_t* out,
+                     bool minimal = true) const {
+        check(ph_gpu_index_stream_kmers(h_, seq, n_bases, k, out, PH_OUT_U32, minimal));
+    }
     // device-resident, asynchronous on `stream`
     void query_device(const uint64_t* d_keys, size_t n, void* d_out, int out_width, bool minimal,
                       ph_gpu_stream_t stream = nullptr) const {

@@ -287,6 +287,76 @@ class Port:
         L.pho_gen_perm_keys.argtypes = [u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                         C.c_uint64]
         L.pho_gen_sample_keys.argtypes = list(L.pho_gen_perm_keys.argtypes)
+        L.pho_gen_dna.argtypes = [u64p, C.c_uint64, C.c_uint64, C.c_uint64]
+        L.pho_kmers.argtypes = [u64p, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, u64p]
+
+    def _threaded(self, count, T, fn):
+        import threading
+        T = T or (os.cpu_count() or 1)
+        step = (count + T - 1) // T
+        ths = [threading.Thread(target=fn, args=(t * step, min(step, count - t * step)))
+               for t in range(T) if t * step < count]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+
+    def gen_strings(self, start: int, count: int, n: int, seed: int, perm_seed: int = 0,
+                    threads: int = 0):
+        """Config-4 strings start..start+count (src = Feistel perm if perm_seed) as one
+        concatenated byte buffer + u64 offsets[count+1] (ph_oracle.c pho_gen_strings)."""
+        import threading
+        self.L.pho_gen_strings.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                           C.c_uint64, u8p, u64p, C.c_uint64]
+        self.L.pho_gen_strings.restype = C.c_uint64
+        T = threads or (os.cpu_count() or 1)
+        step = (count + T - 1) // T
+        parts = [None] * T
+
+        def work(t):
+            b = t * step
+            m = min(step, count - b)
+            if m <= 0:
+                parts[t] = (np.zeros(0, np.uint8), np.zeros(1, np.uint64))
+                return
+            data = np.empty(m * 64, dtype=np.uint8)
+            offs = np.empty(m + 1, dtype=np.uint64)
+            end = self.L.pho_gen_strings(start + b, m, n, seed, perm_seed,
+                                         data.ctypes.data_as(u8p), offs.ctypes.data_as(u64p), 0)
+            parts[t] = (data[:end], offs)
+
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(T)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        total = sum(p[0].size for p in parts)
+        data = np.empty(max(total, 1), dtype=np.uint8)
+        offs = np.empty(count + 1, dtype=np.uint64)
+        pos, k = 0, 0
+        for d, o in parts:
+            m = o.size - 1
+            data[pos:pos + d.size] = d
+            offs[k:k + m + 1] = o + np.uint64(pos)
+            pos += d.size
+            k += m
+        return data, offs
+
+    def gen_dna(self, n_bases: int, seed: int, threads: int = 0) -> np.ndarray:
+        """2-bit packed MSB-first random sequence (ph_gpu.h layout), ceil(n/32) words."""
+        nw = (n_bases + 31) // 32
+        out = np.empty(nw, dtype=np.uint64)
+        self._threaded(nw, threads, lambda b, m: self.L.pho_gen_dna(
+            out[b:].ctypes.data_as(u64p), b, m, seed))
+        return out
+
+    def kmers(self, seq: np.ndarray, n_bases: int, k: int, threads: int = 0) -> np.ndarray:
+        n = n_bases - k + 1
+        out = np.empty(max(n, 0), dtype=np.uint64)
+        seq = np.ascontiguousarray(seq, dtype=np.uint64)
+        self._threaded(n, threads, lambda b, m: self.L.pho_kmers(
+            seq.ctypes.data_as(u64p), n_bases, k, b, m, out[b:].ctypes.data_as(u64p)))
+        return out
 
     def gen_keys(self, kind: str, start: int, count: int, n: int, gen_seed: int, seed: int = 0,
                  threads: int = 0) -> np.ndarray:

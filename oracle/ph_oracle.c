@@ -477,6 +477,51 @@ void pho_gen_sample_keys(uint64_t* out, uint64_t start, uint64_t count, uint64_t
         out[i] = pho_corpus_u64(pho_mix64(sample_seed + (start + i + 1) * kGolden) % n, gen_seed);
 }
 
+/* Config-4 string corpus: string i has len = 8 + r0 % 57 bytes of printable ASCII
+ * 0x21 + mix64(r0 + (t+1)*golden) % 94, with r0 = mix64(seed + (i+1)*golden). Writes the
+ * string into out (>= 64 bytes) and returns its length. */
+uint32_t pho_gen_string(uint64_t i, uint64_t seed, uint8_t* out) {
+    const uint64_t r0 = pho_mix64(seed + (i + 1) * kGolden);
+    const uint32_t len = 8 + (uint32_t)(r0 % 57);
+    for (uint32_t t = 0; t < len; t++) out[t] = (uint8_t)(0x21 + pho_mix64(r0 + (t + 1) * kGolden) % 94);
+    return len;
+}
+/* Strings src(start..start+count) concatenated into data at data_off, offsets[] relative to
+ * data_off's base (offsets[c] is written for c in [0, count]); src = perm(i) if perm_seed != 0. */
+uint64_t pho_gen_strings(uint64_t start, uint64_t count, uint64_t n, uint64_t seed,
+                         uint64_t perm_seed, uint8_t* data, uint64_t* offsets, uint64_t base) {
+    uint64_t pos = base;
+    for (uint64_t c = 0; c < count; c++) {
+        const uint64_t i = start + c;
+        const uint64_t src = perm_seed ? pho_feistel_perm(i, n, perm_seed) : i;
+        offsets[c] = pos;
+        pos += pho_gen_string(src, seed, data + pos);
+    }
+    offsets[count] = pos;
+    return pos;
+}
+
+/* k-mer workload (BASELINE.json config 5; the GPU's fused front end is checked against
+ * this): sequence word w = mix64(seed + (w+1)*golden), bases 2-bit MSB-first (A=0 C=1 G=2
+ * T=3); key i = bases i..i+k-1 with the first base in the most significant bits. */
+void pho_gen_dna(uint64_t* out, uint64_t start_word, uint64_t nwords, uint64_t seed) {
+    for (uint64_t w = 0; w < nwords; w++) out[w] = pho_mix64(seed + (start_word + w + 1) * kGolden);
+}
+void pho_kmers(const uint64_t* seq, uint64_t n_bases, int k, uint64_t start, uint64_t count,
+               uint64_t* out) {
+    for (uint64_t c = 0; c < count; c++) {
+        const uint64_t i = start + c;
+        uint64_t key = 0;
+        for (int t = 0; t < k; t++) { /* base by base, no word tricks */
+            const uint64_t j = i + (uint64_t)t;
+            const uint64_t b = (seq[j / 32] >> (2 * (31 - j % 32))) & 3;
+            key = (key << 2) | b;
+        }
+        (void)n_bases;
+        out[c] = key;
+    }
+}
+
 /* Seeded permutation of [0,n) used as the "shuffled query order" of the
  * synthetic workloads (ours, not the reference's): a 4-round balanced Feistel
  * network over the smallest even-bit domain >= n, with cycle walking. The GPU

@@ -66,6 +66,12 @@ void pho_gen_perm_keys(uint64_t* out, uint64_t start, uint64_t count, uint64_t n
                        uint64_t gen_seed, uint64_t perm_seed);
 void pho_gen_sample_keys(uint64_t* out, uint64_t start, uint64_t count, uint64_t n,
                          uint64_t gen_seed, uint64_t sample_seed);
+void pho_gen_dna(uint64_t* out, uint64_t start_word, uint64_t nwords, uint64_t seed);
+uint32_t pho_gen_string(uint64_t i, uint64_t seed, uint8_t* out);
+uint64_t pho_gen_strings(uint64_t start, uint64_t count, uint64_t n, uint64_t seed,
+                         uint64_t perm_seed, uint8_t* data, uint64_t* offsets, uint64_t base);
+void pho_kmers(const uint64_t* seq, uint64_t n_bases, int k, uint64_t start, uint64_t count,
+               uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -642,6 +642,85 @@ int ph_gpu_index_stream_bytes(const ph_gpu_index* ix, const uint8_t* h_bytes,
     return PH_OK;
 }
 
+int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n_bases, int k,
+                       void* d_out, int out_width, int minimal, ph_gpu_stream_t stream) {
+    if (!ix) return fail(PH_E_INVALID, "null index");
+    if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "k-mer query on a string-key index");
+    if (k < 1 || k > 32) return fail(PH_E_INVALID, "k must be in [1, 32]");
+    if (int rc = check_width(out_width)) return rc;
+    if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
+    if (n_bases < (uint64_t)k) return PH_OK;
+    if (!d_seq || !d_out) return fail(PH_E_INVALID, "null sequence or output pointer");
+    DeviceGuard g(ix->device);
+    cudaError_t e = phg::launch_query_kmers(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_seq,
+                                            n_bases, k, d_out, out_width, minimal,
+                                            static_cast<cudaStream_t>(stream), ix->sms);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "query_kmers launch");
+}
+
+int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uint64_t n_bases,
+                              int k, void* h_out, int out_width, int minimal) {
+    if (!ix) return fail(PH_E_INVALID, "null index");
+    if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "k-mer query on a string-key index");
+    if (k < 1 || k > 32) return fail(PH_E_INVALID, "k must be in [1, 32]");
+    if (int rc = check_width(out_width)) return rc;
+    if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
+    if (n_bases < (uint64_t)k) return PH_OK;
+    if (!h_seq || !h_out) return fail(PH_E_INVALID, "null sequence or output pointer");
+    DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    const uint64_t n = n_bases - (uint64_t)k + 1;  // windows
+    const uint64_t nwords_total = (n_bases + 31) / 32;
+    const size_t C = chunk_keys(n) & ~size_t{31} ? chunk_keys(n) & ~size_t{31} : 32;  // windows
+    const size_t max_words = (C + (size_t)k - 1 + 31) / 32 + 1;
+    const bool bounce = !(is_pinned_host(h_seq) && is_pinned_host(h_out));
+    Pipeline pl;
+    if (int rc = alloc_pipeline(pl, max_words * 8, 0, C * out_width, bounce)) return rc;
+    auto* out_b = static_cast<uint8_t*>(h_out);
+    auto drain = [&](Slot& s) -> int {
+        if (!s.pending) return PH_OK;
+        PH_CUDA(cudaStreamSynchronize(s.s));
+        std::memcpy(out_b + s.pend_off * out_width, s.h_out, s.pend_n * out_width);
+        s.pending = false;
+        return PH_OK;
+    };
+    size_t c = 0;
+    for (uint64_t off = 0; off < n; off += C, c++) {  // off is a multiple of 32
+        Slot& s = pl.slot[c % kSlots];
+        const uint64_t m = n - off < C ? n - off : C;
+        const uint64_t nb = m + (uint64_t)k - 1;  // bases this chunk reads
+        const uint64_t w0 = off / 32;
+        uint64_t nw = (nb + 31) / 32;
+        if (w0 + nw > nwords_total) nw = nwords_total - w0;
+        const void* src = h_seq + w0;
+        void* dst = out_b + off * out_width;
+        if (bounce) {
+            if (int rc = drain(s)) return rc;
+            std::memcpy(s.h_in, h_seq + w0, nw * 8);
+            src = s.h_in;
+            dst = s.h_out;
+        }
+        PH_CUDA(cudaMemcpyAsync(s.d_in, src, nw * 8, cudaMemcpyHostToDevice, s.s));
+        PH_CUDA(phg::launch_query_kmers(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                        static_cast<const uint64_t*>(s.d_in), nb, k, s.d_out,
+                                        out_width, minimal, s.s, ix->sms));
+        PH_CUDA(cudaMemcpyAsync(dst, s.d_out, m * out_width, cudaMemcpyDeviceToHost, s.s));
+        if (bounce) {
+            s.pending = true;
+            s.pend_off = off;
+            s.pend_n = m;
+        }
+    }
+    for (Slot& s : pl.slot) {
+        if (bounce) {
+            if (int rc = drain(s)) return rc;
+        } else {
+            PH_CUDA(cudaStreamSynchronize(s.s));
+        }
+    }
+    return PH_OK;
+}
+
 // Single-key queries: one small device scratch block, synchronous.
 int ph_gpu_index_u64(const ph_gpu_index* ix, uint64_t key, int minimal, uint64_t* out) {
     if (!ix || !out) return fail(PH_E_INVALID, "null argument");

@@ -165,6 +165,53 @@ __global__ void __launch_bounds__(256) k_gather_mode(const uint8_t* __restrict__
     if (acc == 0x7fffffffu) *sink = acc;
 }
 
+// Seeded uniform random ACGT sequence, 2-bit packed MSB-first (ph_gpu.h layout): word w =
+// splitmix64 output w of the stream seeded with `seed`.
+__global__ void k_gen_dna(uint64_t* out, uint64_t nwords, uint64_t seed) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = mix64(seed + (i + 1) * kGolden);
+}
+// Materialised k-mers (first base in the MSBs), the u64 keys the reference builds over.
+__global__ void k_kmers(const uint64_t* __restrict__ seq, uint64_t n_bases, int k, uint64_t* out) {
+    const uint64_t n = n_bases - (uint64_t)k + 1, nwords = (n_bases + 31) / 32;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = i >> 5;
+        const uint32_t o = (uint32_t)(i & 31) * 2;
+        const uint64_t wa = seq[a], wb = (o && a + 1 < nwords) ? seq[a + 1] : 0;
+        const uint64_t top = o ? (wa << o) | (wb >> (64 - o)) : wa;
+        out[i] = k == 32 ? top : top >> (64 - 2 * k);
+    }
+}
+
+// Config-4 string corpus (same definition as oracle/ph_oracle.c pho_gen_string):
+// r0 = mix64(seed + (i+1)*golden); len = 8 + r0 % 57; byte t = 0x21 + mix64(r0 + (t+1)*golden) % 94.
+__device__ __forceinline__ uint64_t str_r0(uint64_t i, uint64_t seed) {
+    return mix64(seed + (i + 1) * kGolden);
+}
+__global__ void k_str_lens(uint64_t* lens, uint64_t n, uint64_t seed, uint64_t perm_seed,
+                           unsigned h, int permuted) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t src = permuted ? feistel(i, n, perm_seed, h) : i;
+        lens[i] = 8 + str_r0(src, seed) % 57;
+    }
+}
+// offsets[i] = start of string i (exclusive scan of lens); writes the bytes of string
+// src(i) (identity or the Feistel permutation) at offsets[i].
+__global__ void k_str_bytes(const uint64_t* __restrict__ offsets, uint64_t n, uint64_t seed,
+                            uint64_t perm_seed, unsigned h, int permuted, uint8_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t src = permuted ? feistel(i, n, perm_seed, h) : i;
+        const uint64_t r0 = str_r0(src, seed);
+        const uint32_t len = 8 + (uint32_t)(r0 % 57);
+        uint8_t* p = out + offsets[i];
+        for (uint32_t t = 0; t < len; t++) p[t] = (uint8_t)(0x21 + mix64(r0 + (t + 1) * kGolden) % 94);
+    }
+}
+
 __global__ void k_bijection(const uint32_t* __restrict__ out, uint64_t count, uint64_t n,
                             unsigned int* bits, unsigned long long* bad) {
     unsigned long long local_oob = 0, local_dup = 0;
@@ -226,6 +273,29 @@ int phb_gather(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t seed,
         case 16: k_gather<16><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
         default: k_gather<8><<<blocks, 256, 0, s>>>(d_buf, F, nloads, seed, d_sink); break;
     }
+    return (int)cudaGetLastError();
+}
+
+int phb_str_lens(uint64_t* d_lens, uint64_t n, uint64_t seed, uint64_t perm_seed, int permuted,
+                 void* stream) {
+    k_str_lens<<<grid(n), 256, 0, (cudaStream_t)stream>>>(d_lens, n, seed, perm_seed,
+                                                        feistel_half_bits(n), permuted);
+    return (int)cudaGetLastError();
+}
+int phb_str_bytes(const uint64_t* d_offsets, uint64_t n, uint64_t seed, uint64_t perm_seed,
+                  int permuted, uint8_t* d_out, void* stream) {
+    k_str_bytes<<<grid(n), 256, 0, (cudaStream_t)stream>>>(d_offsets, n, seed, perm_seed,
+                                                         feistel_half_bits(n), permuted, d_out);
+    return (int)cudaGetLastError();
+}
+
+int phb_gen_dna(uint64_t* d_out, uint64_t nwords, uint64_t seed, void* stream) {
+    k_gen_dna<<<grid(nwords), 256, 0, (cudaStream_t)stream>>>(d_out, nwords, seed);
+    return (int)cudaGetLastError();
+}
+int phb_kmers(const uint64_t* d_seq, uint64_t n_bases, int k, uint64_t* d_out, void* stream) {
+    if (n_bases < (uint64_t)k) return 0;
+    k_kmers<<<grid(n_bases - k + 1), 256, 0, (cudaStream_t)stream>>>(d_seq, n_bases, k, d_out);
     return (int)cudaGetLastError();
 }
 

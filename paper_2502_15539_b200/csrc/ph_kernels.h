@@ -43,6 +43,10 @@ cudaError_t launch_query_bytes(const DevIndex& ix, int gamma_kind, bool pow2,
                                void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                                int sms);
 
+cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* seq,
+                               uint64_t n_bases, int k, void* out, int out_width, int minimal,
+                               cudaStream_t s, int sms);
+
 uint64_t launch_count();
 void note_launch();
 void set_launch(int threads, int bps);

@@ -58,6 +58,10 @@ _L.ph_gpu_index_stream_u64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_v
                                        C.c_int]
 _L.ph_gpu_index_stream_bytes.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                          C.c_void_p, C.c_int, C.c_int]
+_L.ph_gpu_query_kmers.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p,
+                                  C.c_int, C.c_int, C.c_void_p]
+_L.ph_gpu_index_stream_kmers.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p,
+                                         C.c_int, C.c_int]
 _L.ph_gpu_index_u64.argtypes = [C.c_void_p, C.c_uint64, C.c_int, u64p]
 _L.ph_gpu_index_bytes.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, u64p]
 _L.ph_gpu_launch_count.restype = C.c_uint64
@@ -202,6 +206,28 @@ class PtrHashIndex:
         o = out.numpy() if _is_torch(out) else out
         _check(_L.ph_gpu_index_stream_u64(self._h, C.c_void_p(k.ctypes.data), k.size,
                                           C.c_void_p(o.ctypes.data), out_width, int(minimal)))
+        return out
+
+    def query_kmers(self, seq, n_bases: int, k: int = 31, out=None, minimal=True, out_width=4,
+                    stream=None):
+        """Fused k-mer queries: out[i] = index(kmer_i(seq)) for i < n_bases-k+1 (ph_gpu.h
+        ph_gpu_query_kmers). `seq` is the 2-bit packed MSB-first sequence (u64 words)."""
+        n = max(0, n_bases - k + 1)
+        if _is_torch(seq) and seq.is_cuda:
+            import torch
+            if out is None:
+                out = torch.empty(n, dtype=torch.int32 if out_width == 4 else torch.int64,
+                                  device=seq.device)
+            _check(_L.ph_gpu_query_kmers(self._h, C.c_void_p(seq.data_ptr()), n_bases, k,
+                                         C.c_void_p(out.data_ptr()), out_width, int(minimal),
+                                         _stream_ptr(stream)))
+            return out
+        s = seq.numpy() if _is_torch(seq) else np.ascontiguousarray(seq)
+        if out is None:
+            out = np.empty(n, dtype=np.uint32 if out_width == 4 else np.uint64)
+        o = out.numpy() if _is_torch(out) else out
+        _check(_L.ph_gpu_index_stream_kmers(self._h, C.c_void_p(s.ctypes.data), n_bases, k,
+                                            C.c_void_p(o.ctypes.data), out_width, int(minimal)))
         return out
 
     def _query_bytes(self, data, offsets, out, minimal, out_width, stream):

@@ -245,3 +245,46 @@ def test_cpp_wrapper_suite():
     r = subprocess.run([exe, so], capture_output=True, text=True, timeout=600)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr
+
+
+# ---- fused k-mer front end (BASELINE config 5) ----
+
+@pytest.mark.parametrize("k,n_bases", [(31, 200_030), (31, 64_000), (32, 50_017), (16, 40_001),
+                                       (5, 3_001), (1, 100), (31, 31), (31, 30)])
+def test_kmers_fused_vs_reference(ph, ref, port, k, n_bases):
+    seq = port.gen_dna(n_bases, 44 + k)
+    kmers = port.kmers(seq, n_bases, k)
+    if kmers.size == 0:
+        ptrh, _ = load_golden("default_l30")
+        idx = ph.PtrHashIndex(ptrh)
+        assert idx.query_kmers(seq, n_bases, k).size == 0
+        return
+    uniq = np.unique(kmers)
+    ptrh = ref.build_u64(uniq, ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    for minimal in (True, False):
+        want = ri.query_u64(kmers, minimal, "stream", 32, threads=THREADS)
+        d_seq = torch.from_numpy(seq.view(np.int64)).cuda()
+        got = idx.query_kmers(d_seq, n_bases, k, minimal=minimal, out_width=8)
+        torch.cuda.synchronize()
+        assert np.array_equal(host_u(got, 8), want)
+        got_h = idx.query_kmers(seq, n_bases, k, minimal=minimal, out_width=4)
+        assert np.array_equal(got_h.astype(np.uint64), want)
+        # identical to materialising the k-mers and querying them as u64 keys
+        assert np.array_equal(gpu_query(idx, kmers, minimal, 4), want)
+
+
+def test_kmer_harness_matches_oracle(port):
+    import ctypes as C
+    bench = C.CDLL(os.path.join(ROOT, "paper_2502_15539_b200", "libph_bench.so"))
+    n_bases = 100_003
+    seq = port.gen_dna(n_bases, 44)
+    d_seq = torch.empty(seq.size, dtype=torch.int64, device="cuda")
+    bench.phb_gen_dna(C.c_void_p(d_seq.data_ptr()), C.c_uint64(seq.size), C.c_uint64(44), None)
+    assert np.array_equal(d_seq.cpu().numpy().view(np.uint64), seq)
+    for k in (31, 32, 7):
+        out = torch.empty(n_bases - k + 1, dtype=torch.int64, device="cuda")
+        bench.phb_kmers(C.c_void_p(d_seq.data_ptr()), C.c_uint64(n_bases), k,
+                        C.c_void_p(out.data_ptr()), None)
+        assert np.array_equal(host_u(out, 8), port.kmers(seq, n_bases, k))

@@ -214,3 +214,18 @@ def test_feistel_is_a_permutation(port):
     for n in (1, 2, 3, 1000, 4097, 65536):
         p = [port.L.pho_feistel_perm(i, n, 7) for i in range(n)]
         assert sorted(p) == list(range(n))
+
+
+def test_kmer_oracle_matches_numpy(port):
+    n_bases = 5_003
+    seq = port.gen_dna(n_bases, 44)
+    bases = np.array([(int(seq[j // 32]) >> (2 * (31 - j % 32))) & 3 for j in range(n_bases)])
+    for k in (1, 5, 31, 32):
+        want = []
+        for i in range(0, n_bases - k + 1, 97):
+            v = 0
+            for t in range(k):
+                v = (v << 2) | int(bases[i + t])
+            want.append(v)
+        got = port.kmers(seq, n_bases, k)[::97]
+        assert [int(x) for x in got] == want

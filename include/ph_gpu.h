@@ -116,6 +116,13 @@ int ph_gpu_index_bytes(const ph_gpu_index* index, const uint8_t* key, size_t len
 /* ---- introspection ---- */
 /* Number of query-kernel launches this process made through this library. */
 uint64_t ph_gpu_launch_count(void);
+/* Minimal queries of at least min_keys keys (default 2^20) defer the slot >= n remap to a
+ * second kernel (warp-private lists + k_remap_patch); smaller ones remap inline.
+ * UINT64_MAX disables deferral. Results are identical either way. */
+int ph_gpu_set_defer_min(uint64_t min_keys);
+/* Kernel tuning for u64/k-mer queries: 0 = automatic (by pilot bytes vs L2), 1 = the
+ * L2-resident tuning, 2 = the DRAM-bound tuning. Tuning/bench knob. */
+int ph_gpu_set_regime(int regime);
 /* Override the bulk-kernel launch shape (0 = automatic). For tuning/bench. */
 int ph_gpu_set_launch(int threads_per_block, int blocks_per_sm);
 /* Pilot-gather L2 policy (default: hot_bytes = 64 MiB, flags = 0). The device copy of

@@ -10,6 +10,7 @@
 //    (pipelined H2D -> kernel -> D2H over chunks and streams, synchronous).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -108,6 +109,7 @@ struct ph_gpu_index {
     void* d_remap = nullptr;
     void* d_ef[3] = {nullptr, nullptr, nullptr};
     void* d_opt = nullptr;
+    cudaMemPool_t pool = nullptr;  // stream-ordered scratch for the deferred remap
 };
 
 namespace {
@@ -263,8 +265,38 @@ void release(ph_gpu_index* ix) {
     cudaFree(ix->d_remap);
     for (void* p : ix->d_ef) cudaFree(p);
     cudaFree(ix->d_opt);
+    if (ix->pool) cudaMemPoolDestroy(ix->pool);
     delete ix;
 }
+
+// Stream-ordered scratch for the deferred remap list of one launch: used
+// for minimal queries of at least kDeferMin keys; capacity n/32 + 64 Ki entries (3x the
+// 1% remap rate of alpha = 0.99; overflow entries are decoded inline, never dropped).
+std::atomic<uint64_t> g_defer_min{uint64_t{1} << 20};  // ph_gpu_set_defer_min
+
+struct DeferScratch {
+    phg::RemapList rl{nullptr, nullptr, nullptr, 0};
+    void* p = nullptr;
+    cudaStream_t s;
+    DeferScratch(const ph_gpu_index* ix, uint64_t n, int minimal, cudaStream_t stream) : s(stream) {
+        if (!minimal || n < g_defer_min.load() || !ix->pool) return;
+        const uint64_t cap = n / 32 + 65536;
+        const size_t counts_bytes = size_t{phg::kMaxRemapLists} * 4;
+        if (cudaMallocFromPoolAsync(&p, counts_bytes + cap * 16, ix->pool, s) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return;  // inline remap
+        }
+        auto* b = static_cast<uint8_t*>(p);
+        rl.counts = reinterpret_cast<uint32_t*>(b);  // every grid warp writes its count
+        rl.idx = reinterpret_cast<uint64_t*>(b + counts_bytes);
+        rl.rem = rl.idx + cap;
+        rl.cap = cap;
+    }
+    ~DeferScratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
 
 int check_width(int w) {
     return (w == PH_OUT_U32 || w == PH_OUT_U64) ? PH_OK
@@ -302,6 +334,15 @@ extern "C" {
 
 const char* ph_gpu_last_error(void) { return g_err.c_str(); }
 uint64_t ph_gpu_launch_count(void) { return phg::launch_count(); }
+int ph_gpu_set_regime(int regime) {
+    if (regime < 0 || regime > 2) return fail(PH_E_INVALID, "regime must be 0, 1 or 2");
+    phg::set_regime(regime);
+    return PH_OK;
+}
+int ph_gpu_set_defer_min(uint64_t min_keys) {
+    g_defer_min.store(min_keys);
+    return PH_OK;
+}
 int ph_gpu_set_launch(int threads, int bps) {
     if (threads != 0 && (threads < 32 || threads > 1024 || threads % 32))
         return fail(PH_E_INVALID, "threads_per_block must be a multiple of 32 in [32,1024]");
@@ -388,6 +429,19 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
     d.remap_kind = p.remap_kind;
     d.ef_low_bits = p.ef_low_bits;
     d.hash_algo = p.algo;
+    {  // per-index memory pool for per-call scratch (kept cached between calls)
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        if (cudaMemPoolCreate(&ix->pool, &props) == cudaSuccess) {
+            uint64_t keep = ~uint64_t{0};
+            cudaMemPoolSetAttribute(ix->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        } else {
+            cudaGetLastError();
+            ix->pool = nullptr;  // no deferral: inline remap only
+        }
+    }
     *out = ix;
     return PH_OK;
 }
@@ -431,9 +485,10 @@ int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, v
     if (n == 0) return PH_OK;
     if (!d_keys || !d_out) return fail(PH_E_INVALID, "null key or output pointer");
     DeviceGuard g(ix->device);
+    DeferScratch ds(ix, n, minimal, static_cast<cudaStream_t>(stream));
     cudaError_t e = phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_keys, d_out,
                                           out_width, n, minimal, static_cast<cudaStream_t>(stream),
-                                          ix->sms);
+                                          ix->sms, ds.rl);
     return e == cudaSuccess ? PH_OK : cuda_fail(e, "query_u64 launch");
 }
 
@@ -553,9 +608,12 @@ int ph_gpu_index_stream_u64(const ph_gpu_index* ix, const uint64_t* h_keys, size
             dst = s.h_out;
         }
         PH_CUDA(cudaMemcpyAsync(s.d_in, src, m * 8, cudaMemcpyHostToDevice, s.s));
-        PH_CUDA(phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2,
-                                      static_cast<const uint64_t*>(s.d_in), s.d_out, out_width, m,
-                                      minimal, s.s, ix->sms));
+        {
+            DeferScratch ds(ix, m, minimal, s.s);
+            PH_CUDA(phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                          static_cast<const uint64_t*>(s.d_in), s.d_out, out_width,
+                                          m, minimal, s.s, ix->sms, ds.rl));
+        }
         PH_CUDA(cudaMemcpyAsync(dst, s.d_out, m * out_width, cudaMemcpyDeviceToHost, s.s));
         if (bounce) {
             s.pending = true;
@@ -652,9 +710,10 @@ int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n
     if (n_bases < (uint64_t)k) return PH_OK;
     if (!d_seq || !d_out) return fail(PH_E_INVALID, "null sequence or output pointer");
     DeviceGuard g(ix->device);
+    DeferScratch ds(ix, n_bases - (uint64_t)k + 1, minimal, static_cast<cudaStream_t>(stream));
     cudaError_t e = phg::launch_query_kmers(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_seq,
                                             n_bases, k, d_out, out_width, minimal,
-                                            static_cast<cudaStream_t>(stream), ix->sms);
+                                            static_cast<cudaStream_t>(stream), ix->sms, ds.rl);
     return e == cudaSuccess ? PH_OK : cuda_fail(e, "query_kmers launch");
 }
 
@@ -701,9 +760,12 @@ int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uin
             dst = s.h_out;
         }
         PH_CUDA(cudaMemcpyAsync(s.d_in, src, nw * 8, cudaMemcpyHostToDevice, s.s));
-        PH_CUDA(phg::launch_query_kmers(ix->dev, ix->info.bucket_fn, ix->info.pow2,
-                                        static_cast<const uint64_t*>(s.d_in), nb, k, s.d_out,
-                                        out_width, minimal, s.s, ix->sms));
+        {
+            DeferScratch ds(ix, m, minimal, s.s);
+            PH_CUDA(phg::launch_query_kmers(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                            static_cast<const uint64_t*>(s.d_in), nb, k, s.d_out,
+                                            out_width, minimal, s.s, ix->sms, ds.rl));
+        }
         PH_CUDA(cudaMemcpyAsync(dst, s.d_out, m * out_width, cudaMemcpyDeviceToHost, s.s));
         if (bounce) {
             s.pending = true;

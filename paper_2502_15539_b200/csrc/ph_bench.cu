@@ -212,6 +212,74 @@ __global__ void k_str_bytes(const uint64_t* __restrict__ offsets, uint64_t n, ui
     }
 }
 
+// Die probe (dual-die L2 study): one thread times a dependent ld.global.cv of the first
+// word of each `chunk`-byte block of buf (after a warming pass), recording latency cycles
+// and the SM it ran on. Bimodal latencies = near/far home L2.
+__global__ void k_die_probe(const uint32_t* buf, uint64_t nchunks, uint32_t chunk_words,
+                            uint32_t* lat, uint32_t* smid_out, int passes) {
+    __shared__ volatile uint32_t sink_s;
+    if (threadIdx.x != 0) return;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid_out) smid_out[blockIdx.x] = smid;
+    uint32_t v = 1;
+    // windows of 4096 chunks (8 MiB at 2 KiB) so the warm pass leaves them L2-resident
+    for (uint64_t w0 = 0; w0 < nchunks; w0 += 4096) {
+        const uint64_t w1 = w0 + 4096 < nchunks ? w0 + 4096 : nchunks;
+        for (int p = 0; p < passes; p++) {
+            for (uint64_t c = w0; c < w1; c++) {
+                // buf holds ones: (v - 1) == 0 chains each address on the previous load
+                const uint32_t* a = buf + c * chunk_words + (v - 1);
+                long long t0, t1;
+                asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
+                asm volatile("ld.global.cv.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+                sink_s = v;  // the store waits for the load; clock is read after it issues
+                asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1));
+                if (p == passes - 1) lat[blockIdx.x * nchunks + c] = (uint32_t)(t1 - t0);
+            }
+        }
+    }
+}
+
+// Die-aware gather: a thread on an SM of die d loads random bytes from random chunks of
+// list d (chunk_off[d][0..nch[d]) in bytes). sm_die[smid] gives the die of each SM.
+// mode 0: die-local lists; mode 1: both lists mixed (control, same footprint).
+__global__ void __launch_bounds__(256) k_gather_die(const uint8_t* __restrict__ buf,
+                                                    const uint32_t* __restrict__ list0,
+                                                    uint32_t n0,
+                                                    const uint32_t* __restrict__ list1,
+                                                    uint32_t n1, const int8_t* __restrict__ sm_die,
+                                                    uint32_t chunk, uint64_t nloads, uint64_t seed,
+                                                    int mode, uint32_t* sink) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int d = sm_die[smid];
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 8;
+    uint32_t acc = 0;
+    for (uint64_t base = tid * 8; base < nloads; base += stride) {
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t r = mix64(seed + (base + j) * kGolden);
+            int dd = mode == 0 ? d : (int)(r >> 63);
+            const uint32_t* L = dd ? list1 : list0;
+            const uint32_t n = dd ? n1 : n0;
+            const uint32_t c = (uint32_t)__umul64hi(r & 0x7fffffffffffffffull, (uint64_t)n << 1);
+            const uint64_t a = (uint64_t)__ldg(L + c) * chunk + ((uint32_t)r % chunk);
+            uint16_t x;
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+                         : "=h"(x) : "l"(buf + a), "l"(pol));
+            v[j] = x;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc += v[j];
+    }
+    if (acc == 0x7fffffffu) *sink = acc;
+}
+
 __global__ void k_bijection(const uint32_t* __restrict__ out, uint64_t count, uint64_t n,
                             unsigned int* bits, unsigned long long* bad) {
     unsigned long long local_oob = 0, local_dup = 0;
@@ -286,6 +354,23 @@ int phb_str_bytes(const uint64_t* d_offsets, uint64_t n, uint64_t seed, uint64_t
                   int permuted, uint8_t* d_out, void* stream) {
     k_str_bytes<<<grid(n), 256, 0, (cudaStream_t)stream>>>(d_offsets, n, seed, perm_seed,
                                                          feistel_half_bits(n), permuted, d_out);
+    return (int)cudaGetLastError();
+}
+
+int phb_die_probe(const uint32_t* d_buf, uint64_t nchunks, uint32_t chunk_bytes, int blocks,
+                  uint32_t* d_lat, uint32_t* d_smid, int passes, void* stream) {
+    k_die_probe<<<blocks, 32, 0, (cudaStream_t)stream>>>(d_buf, nchunks, chunk_bytes / 4, d_lat,
+                                                        d_smid, passes);
+    return (int)cudaGetLastError();
+}
+
+int phb_gather_die(const uint8_t* d_buf, const uint32_t* l0, uint32_t n0, const uint32_t* l1,
+                   uint32_t n1, const int8_t* sm_die, uint32_t chunk, uint64_t nloads,
+                   uint64_t seed, int mode, uint32_t* d_sink, void* stream) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    k_gather_die<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(d_buf, l0, n0, l1, n1, sm_die, chunk,
+                                                           nloads, seed, mode, d_sink);
     return (int)cudaGetLastError();
 }
 

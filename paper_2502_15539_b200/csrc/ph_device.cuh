@@ -227,4 +227,25 @@ __device__ __forceinline__ uint64_t remap_get(const DevIndex& ix, uint64_t idx) 
     return ef_get(ix, idx);
 }
 
+// The same decode as an out-of-line call, for the query kernels' rare paths: keeps the
+// decode's registers out of the hot loop's allocation (occupancy).
+static __device__ __noinline__ uint64_t remap_get_call(const uint8_t* remap,
+                                                      const uint64_t* ef_low,
+                                                      const uint64_t* ef_high,
+                                                      const uint64_t* ef_samples, int kind,
+                                                      int low_bits, uint64_t idx) {
+    DevIndex v;
+    v.remap = remap;
+    v.ef_low = ef_low;
+    v.ef_high = ef_high;
+    v.ef_samples = ef_samples;
+    v.remap_kind = kind;
+    v.ef_low_bits = low_bits;
+    return remap_get(v, idx);
+}
+__device__ __forceinline__ uint64_t remap_get_cold(const DevIndex& ix, uint64_t idx) {
+    return remap_get_call(ix.remap, ix.ef_low, ix.ef_high, ix.ef_samples, ix.remap_kind,
+                          ix.ef_low_bits, idx);
+}
+
 }  // namespace phg

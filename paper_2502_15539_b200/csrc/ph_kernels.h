@@ -34,9 +34,20 @@ inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsig
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// Scratch for the deferred remap (k_remap_patch); idx == nullptr selects the inline
+// warp-compacted remap instead. Every warp of the query grid owns a private list of
+// cap / (grid warps) entries (no atomics) and writes its count to counts[warp].
+struct RemapList {
+    uint64_t* idx;
+    uint64_t* rem;
+    uint32_t* counts;   // >= kMaxRemapLists entries
+    uint64_t cap;       // total entries
+};
+constexpr uint32_t kMaxRemapLists = 1u << 16;
+
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
-                             int sms);
+                             int sms, const RemapList& rl = RemapList{nullptr, nullptr, nullptr, 0});
 
 cudaError_t launch_query_bytes(const DevIndex& ix, int gamma_kind, bool pow2,
                                const uint8_t* bytes, const uint64_t* offsets, uint64_t base_off,
@@ -45,10 +56,12 @@ cudaError_t launch_query_bytes(const DevIndex& ix, int gamma_kind, bool pow2,
 
 cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* seq,
                                uint64_t n_bases, int k, void* out, int out_width, int minimal,
-                               cudaStream_t s, int sms);
+                               cudaStream_t s, int sms,
+                               const RemapList& rl = RemapList{nullptr, nullptr, nullptr, 0});
 
 uint64_t launch_count();
 void note_launch();
 void set_launch(int threads, int bps);
+void set_regime(int r);
 
 }  // namespace phg

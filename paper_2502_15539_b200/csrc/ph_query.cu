@@ -23,18 +23,17 @@
 
 namespace phg {
 
-#ifndef PH_KPT
-#define PH_KPT 8
-#endif
+// Compile-time switches for tools/tune.py variant builds (keys per thread and CTAs per SM
+// are per-regime template parameters, see launch_u64_t).
 #ifndef PH_PIPE
 #define PH_PIPE 1
 #endif
-// CTA size and the register-bounding minimum CTAs per SM (tools/tune.py sweeps)
+// deferred remap (warp-private lists + k_remap_patch) compiled in
+#ifndef PH_DEFER
+#define PH_DEFER 1
+#endif
 #ifndef PH_THREADS
 #define PH_THREADS 128
-#endif
-#ifndef PH_MINB
-#define PH_MINB 1
 #endif
 
 // Warp-cooperative remap of the keys flagged in need[] (slot >= n).
@@ -96,12 +95,65 @@ __device__ __forceinline__ uint64_t kmer_at(const uint64_t* __restrict__ seq, ui
 // SRC = 0: keys[] is an array of u64 keys. SRC = 1: keys[] is a 2-bit packed sequence of
 // seq_words words and key i is its i-th k-mer (kbits = 2k) — the fused streaming front
 // end for k-mer workloads: 0.25 B/query of input instead of 8 B.
-template <int G, bool POW2, class OutT, int KPT, int SRC>
-__global__ void __launch_bounds__(PH_THREADS, PH_MINB) k_query_u64(const DevIndex ix,
+// Deferred remap: the keys with slot >= n are appended to the warp's private list and
+// decoded by k_remap_patch after the main kernel, so the dependent remap read leaves the
+// main kernel's critical path (no third serial memory latency per tile). Ranks come from
+// the same ballots as the inline path; the warp's running count stays in a register (no
+// atomics). Entries beyond the list's capacity are decoded inline, never dropped.
+template <int KPT, class OutT>
+__device__ __forceinline__ void defer_tile(const DevIndex& ix, uint64_t* __restrict__ lidx,
+                                           uint64_t* __restrict__ lrem, uint32_t lcap,
+                                           uint32_t& wcount, const bool (&need)[KPT],
+                                           uint64_t (&slot)[KPT], uint64_t base) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1;
+    unsigned m[KPT];
+    uint32_t total = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+        m[j] = __ballot_sync(kFull, need[j]);
+        total += __popc(m[j]);
+    }
+    if (total == 0) return;                 // warp-uniform
+    if (wcount + total > lcap) {            // list full: decode this tile inline
+        remap_tile<KPT, OutT>(ix, need, slot);
+        return;
+    }
+    uint32_t pos = wcount;
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+        if (need[j]) {
+            const uint32_t p = pos + __popc(m[j] & lt_mask);
+            lidx[p] = base + (uint64_t)j * 32 + lane;
+            lrem[p] = slot[j] - ix.n;
+        }
+        pos += __popc(m[j]);
+    }
+    wcount = pos;
+}
+
+// One warp per list: decode its entries and patch the outputs.
+template <class OutT>
+__global__ void __launch_bounds__(256) k_remap_patch(const DevIndex ix, const RemapList rl,
+                                                     uint32_t nlists, OutT* __restrict__ out) {
+    const uint32_t lcap = (uint32_t)(rl.cap / nlists);
+    const unsigned lane = threadIdx.x & 31;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nlists;
+         w += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t c = min(rl.counts[w], lcap);
+        const uint64_t* li = rl.idx + (uint64_t)w * lcap;
+        const uint64_t* lr = rl.rem + (uint64_t)w * lcap;
+        for (uint32_t e = lane; e < c; e += 32)
+            out[li[e]] = (OutT)remap_get(ix, lr[e]);  // remap_slot, index.hpp:98-100
+    }
+}
+
+template <int G, bool POW2, class OutT, int KPT, int SRC, int MINB>
+__global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex ix,
                                                    const uint64_t* __restrict__ keys,
                                                    OutT* __restrict__ out, uint64_t nkeys,
                                                    int minimal, uint64_t seq_words,
-                                                   uint32_t kbits) {
+                                                   uint32_t kbits, const RemapList rl) {
     constexpr uint64_t kTile = 32ull * KPT;
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -111,6 +163,11 @@ __global__ void __launch_bounds__(PH_THREADS, PH_MINB) k_query_u64(const DevInde
 
     const uint64_t stride = nwarps * kTile;
     const uint32_t P32 = (uint32_t)ix.P, B32 = (uint32_t)ix.B, S32 = (uint32_t)ix.S;
+    // deferred-remap list of this warp (when rl.idx != nullptr)
+    const uint32_t lcap = rl.idx ? (uint32_t)(rl.cap / nwarps) : 0;
+    uint64_t* lidx = rl.idx ? rl.idx + warp * lcap : nullptr;
+    uint64_t* lrem = rl.idx ? rl.rem + warp * lcap : nullptr;
+    uint32_t wcount = 0;
     // PH_PIPE: the next tile's keys are loaded before this tile's pilot gather and remap,
     // so the key stream's DRAM latency overlaps them (software pipelining across tiles).
     uint64_t knext[KPT];
@@ -168,12 +225,16 @@ __global__ void __launch_bounds__(PH_THREADS, PH_MINB) k_query_u64(const DevInde
             slot[j] = (uint64_t)part[j] * S32 + reduce<POW2>(ix, h[j] ^ hash_pilot(ix, pilot[j]));
             need[j] = minimal && slot[j] >= ix.n && (uint32_t)(j * 32) + lane < rem;
         }
-        if (minimal) remap_tile<KPT, OutT>(ix, need, slot);  // remap_slot, index.hpp:98-100
+        if (minimal) {  // remap_slot, index.hpp:98-100
+            if (PH_DEFER && rl.idx) defer_tile<KPT, OutT>(ix, lidx, lrem, lcap, wcount, need, slot, base);
+            else remap_tile<KPT, OutT>(ix, need, slot);
+        }
         OutT* op = out + base + lane;
 #pragma unroll
         for (int j = 0; j < KPT; j++)
             if ((uint32_t)(j * 32) + lane < rem) st_stream(op + j * 32, slot[j]);
     }
+    if (PH_DEFER && rl.idx && lane == 0) rl.counts[warp] = wcount;
 }
 
 // ---------------------------------------------------------------------------
@@ -213,26 +274,56 @@ struct KeySrc {
     uint32_t kbits;
 };
 
-template <int G, bool POW2, class OutT, int SRC>
-static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
-                                int minimal, cudaStream_t s, int sms) {
-    constexpr int KPT = PH_KPT;
-    auto kern = k_query_u64<G, POW2, OutT, KPT, SRC>;
+// Two tunings of the same kernel, chosen per index by the pilot array's size
+// (tools/tune.py sweeps):
+//  * DRAM regime (pilots > kDramRegimeBytes, e.g. configs 3/5): the pilot gather is bound
+//    by DRAM row activations; KPT=8 with the compiler's register allocation (12 warps/SM)
+//    and the inline warp-compacted remap measured fastest;
+//  * L2 regime (pilots L2-resident, configs 1/2): latency-bound; KPT=4 at 8 CTAs/SM
+//    (32 warps/SM) with the remap deferred to k_remap_patch measured fastest.
+constexpr uint64_t kDramRegimeBytes = uint64_t{64} << 20;
+static int g_regime = 0;  // 0 auto, 1 force L2 regime, 2 force DRAM regime
+void set_regime(int r) { g_regime = r; }
+
+template <int G, bool POW2, class OutT, int SRC, int KPT, int MINB, bool DEFER>
+static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
+                                int minimal, cudaStream_t s, int sms, const RemapList& rl) {
+    auto kern = k_query_u64<G, POW2, OutT, KPT, SRC, MINB>;
     const int threads = g_threads_override > 0 ? g_threads_override : PH_THREADS;
     const int blocks = grid_for(kern, threads, (uint64_t)threads / 32 * 32 * KPT, n, sms);
-    const cudaError_t e = launch_ex(ix, kern, blocks, threads, s, ix, src.ptr,
-                                    static_cast<OutT*>(out), n, minimal, src.seq_words, src.kbits);
+    const uint32_t nlists = (uint32_t)blocks * (uint32_t)(threads / 32);
+    const RemapList use = (PH_DEFER && DEFER && minimal && rl.idx && nlists <= kMaxRemapLists &&
+                           rl.cap / nlists >= 32)
+                              ? rl
+                              : RemapList{nullptr, nullptr, nullptr, 0};
+    cudaError_t e = launch_ex(ix, kern, blocks, threads, s, ix, src.ptr, static_cast<OutT*>(out),
+                              n, minimal, src.seq_words, src.kbits, use);
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e == cudaSuccess && use.idx) {
+        k_remap_patch<OutT><<<(nlists + 7) / 8, 256, 0, s>>>(ix, use, nlists,
+                                                              static_cast<OutT*>(out));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+    }
     return e;
+}
+
+template <int G, bool POW2, class OutT, int SRC>
+static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
+                                int minimal, cudaStream_t s, int sms, const RemapList& rl) {
+    const bool dram = g_regime == 2 || (g_regime == 0 && ix.P * ix.B > kDramRegimeBytes);
+    if (dram) return launch_u64_k<G, POW2, OutT, SRC, 8, 1, false>(ix, src, out, n, minimal, s, sms, rl);
+    return launch_u64_k<G, POW2, OutT, SRC, 4, 8, true>(ix, src, out, n, minimal, s, sms, rl);
 }
 
 template <class OutT, int SRC>
 static cudaError_t launch_u64_w(const DevIndex& ix, int gamma_kind, bool pow2, const KeySrc& k,
-                                void* o, uint64_t n, int minimal, cudaStream_t s, int sms) {
-#define PH_CASE(G)                                                                      \
-    case G:                                                                             \
-        return pow2 ? launch_u64_t<G, true, OutT, SRC>(ix, k, o, n, minimal, s, sms)  \
-                    : launch_u64_t<G, false, OutT, SRC>(ix, k, o, n, minimal, s, sms);
+                                void* o, uint64_t n, int minimal, cudaStream_t s, int sms,
+                                const RemapList& rl) {
+#define PH_CASE(G)                                                                          \
+    case G:                                                                                 \
+        return pow2 ? launch_u64_t<G, true, OutT, SRC>(ix, k, o, n, minimal, s, sms, rl)  \
+                    : launch_u64_t<G, false, OutT, SRC>(ix, k, o, n, minimal, s, sms, rl);
     switch (gamma_kind) {
         PH_CASE(0)
         PH_CASE(1)
@@ -246,31 +337,31 @@ static cudaError_t launch_u64_w(const DevIndex& ix, int gamma_kind, bool pow2, c
 
 static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, const KeySrc& k,
                               void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
-                              int sms) {
+                              int sms, const RemapList& rl) {
     if (n == 0) return cudaSuccess;
     if (k.kind == 1)
         return out_width == 4
-                   ? launch_u64_w<uint32_t, 1>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms)
-                   : launch_u64_w<uint64_t, 1>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms);
+                   ? launch_u64_w<uint32_t, 1>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl)
+                   : launch_u64_w<uint64_t, 1>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl);
     return out_width == 4
-               ? launch_u64_w<uint32_t, 0>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms)
-               : launch_u64_w<uint64_t, 0>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms);
+               ? launch_u64_w<uint32_t, 0>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl)
+               : launch_u64_w<uint64_t, 0>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl);
 }
 
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
-                             int sms) {
+                             int sms, const RemapList& rl) {
     return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0}, out, out_width, n, minimal, s,
-                      sms);
+                      sms, rl);
 }
 
 cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* seq,
                                uint64_t n_bases, int k, void* out, int out_width, int minimal,
-                               cudaStream_t s, int sms) {
+                               cudaStream_t s, int sms, const RemapList& rl) {
     if (n_bases < (uint64_t)k) return cudaSuccess;
     const uint64_t n = n_bases - (uint64_t)k + 1;
     return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k)},
-                      out, out_width, n, minimal, s, sms);
+                      out, out_width, n, minimal, s, sms, rl);
 }
 
 }  // namespace phg

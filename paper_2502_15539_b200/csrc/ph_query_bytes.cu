@@ -40,9 +40,13 @@ __constant__ uint8_t c_sbox[256] = {
     0xe1, 0xf8, 0x98, 0x11, 0x69, 0xd9, 0x8e, 0x94, 0x9b, 0x1e, 0x87, 0xe9, 0xce, 0x55, 0x28, 0xdf,
     0x8c, 0xa1, 0x89, 0x0d, 0xbf, 0xe6, 0x42, 0x68, 0x41, 0x99, 0x2d, 0x0f, 0xb0, 0x54, 0xbb, 0x16};
 
+// One MixColumns∘SubBytes table T0[x] = (2·S[x], S[x], S[x], 3·S[x]) (rows 0..3, LE), held
+// in shared memory 32 times, interleaved so that entry x of copy `lane` sits at word
+// x*32 + lane: every lane reads its own copy, i.e. its own bank, so the 16 lookups of an
+// AES round are conflict-free whatever the state bytes are. The rows' rotated tables are
+// T0 rotated by 8/16/24 bits, and S[x] is byte 1 of T0[x] (for AESENCLAST).
 struct AesTables {
-    uint32_t t[4][256];  // MixColumns∘SubBytes columns, rotated per row
-    uint32_t s[256];     // plain S-box (aesenclast)
+    uint32_t t0[256 * 32];  // 32 KiB
 };
 
 __device__ __forceinline__ uint8_t xtime(uint8_t a) {
@@ -50,59 +54,74 @@ __device__ __forceinline__ uint8_t xtime(uint8_t a) {
 }
 
 __device__ void fill_tables(AesTables& T) {
-    for (int x = threadIdx.x; x < 256; x += blockDim.x) {
+    for (int e = threadIdx.x; e < 256 * 32; e += blockDim.x) {
+        const int x = e >> 5;
         const uint8_t s = c_sbox[x];
         const uint8_t s2 = xtime(s), s3 = (uint8_t)(s2 ^ s);
-        const uint32_t t0 = (uint32_t)s2 | ((uint32_t)s << 8) | ((uint32_t)s << 16) | ((uint32_t)s3 << 24);
-        T.t[0][x] = t0;
-        T.t[1][x] = __funnelshift_l(t0, t0, 8);
-        T.t[2][x] = __funnelshift_l(t0, t0, 16);
-        T.t[3][x] = __funnelshift_l(t0, t0, 24);
-        T.s[x] = s;
+        T.t0[e] = (uint32_t)s2 | ((uint32_t)s << 8) | ((uint32_t)s << 16) | ((uint32_t)s3 << 24);
     }
 }
 
 // state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
 // in-memory byte order of the __m128i in hash.cpp. AESENC = ShiftRows,
-// SubBytes, MixColumns, AddRoundKey (Intel semantics).
+// SubBytes, MixColumns, AddRoundKey (Intel semantics). Tl = T.t0 + lane.
+__device__ __forceinline__ uint32_t tl(const uint32_t* Tl, uint32_t byte) { return Tl[byte << 5]; }
+
 __device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4],
-                                       const AesTables& T) {
+                                       const uint32_t* Tl) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        o[c] = T.t[0][s[c] & 0xff] ^ T.t[1][(s[(c + 1) & 3] >> 8) & 0xff] ^
-               T.t[2][(s[(c + 2) & 3] >> 16) & 0xff] ^ T.t[3][s[(c + 3) & 3] >> 24] ^ k[c];
+        const uint32_t a0 = tl(Tl, s[c] & 0xff);
+        const uint32_t a1 = tl(Tl, (s[(c + 1) & 3] >> 8) & 0xff);
+        const uint32_t a2 = tl(Tl, (s[(c + 2) & 3] >> 16) & 0xff);
+        const uint32_t a3 = tl(Tl, s[(c + 3) & 3] >> 24);
+        o[c] = a0 ^ __funnelshift_l(a1, a1, 8) ^ __funnelshift_l(a2, a2, 16) ^
+               __funnelshift_l(a3, a3, 24) ^ k[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
 }
+__device__ __forceinline__ uint32_t sbox(const uint32_t* Tl, uint32_t byte) {
+    return (tl(Tl, byte) >> 8) & 0xff;
+}
 __device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)[4],
-                                           const AesTables& T) {
+                                           const uint32_t* Tl) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        o[c] = (T.s[s[c] & 0xff] | (T.s[(s[(c + 1) & 3] >> 8) & 0xff] << 8) |
-                (T.s[(s[(c + 2) & 3] >> 16) & 0xff] << 16) | (T.s[s[(c + 3) & 3] >> 24] << 24)) ^
+        o[c] = (sbox(Tl, s[c] & 0xff) | (sbox(Tl, (s[(c + 1) & 3] >> 8) & 0xff) << 8) |
+                (sbox(Tl, (s[(c + 2) & 3] >> 16) & 0xff) << 16) |
+                (sbox(Tl, s[(c + 3) & 3] >> 24) << 24)) ^
                k[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
 }
 
-// Loads min(avail,16) bytes at base+off as 4 LE words, zero past `avail`.
-// Only aligned 4-byte words that hold at least one requested byte are read,
-// so no access leaves the 4-byte words covering the key.
+// Loads min(avail,16) bytes at base+off as 4 LE words, zero past `avail`, with at most
+// two aligned 16-byte loads. Only aligned 16-byte granules that hold at least one
+// requested byte are read, so no access leaves the granules covering the key.
 __device__ __forceinline__ void load16(const uint8_t* __restrict__ base, uint64_t off,
                                        uint32_t avail, uint32_t (&w)[4]) {
-    const uint64_t a = off & ~3ull;
-    const uint32_t sh = (uint32_t)(off & 3) * 8;
-    const uint32_t* p = reinterpret_cast<const uint32_t*>(base + a);
-    const uint64_t end = off + (avail < 16 ? avail : 16);
-    uint32_t r[5];
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(base + off);
+    const uint4* p = reinterpret_cast<const uint4*>(addr & ~uintptr_t{15});
+    const uint32_t sh = (uint32_t)(addr & 15);
+    const uint32_t nb = avail < 16 ? avail : 16;
+    const uint4 lo = __ldg(p);
+    const uint4 hi = (sh + nb > 16) ? __ldg(p + 1) : make_uint4(0, 0, 0, 0);
+    uint32_t r[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    if (sh & 8) {
 #pragma unroll
-    for (int t = 0; t < 5; t++) r[t] = (a + 4 * t < end) ? __ldg(p + t) : 0u;
+        for (int t = 0; t < 6; t++) r[t] = r[t + 2];
+    }
+    if (sh & 4) {
 #pragma unroll
-    for (int t = 0; t < 4; t++) w[t] = __funnelshift_r(r[t], r[t + 1], sh);
+        for (int t = 0; t < 7; t++) r[t] = r[t + 1];
+    }
+    const uint32_t rb = (sh & 3) * 8;
+#pragma unroll
+    for (int t = 0; t < 4; t++) w[t] = __funnelshift_r(r[t], r[t + 1], rb);
     if (avail < 16) {
 #pragma unroll
         for (int t = 0; t < 4; t++) {
@@ -174,7 +193,7 @@ __device__ __forceinline__ void set128(uint32_t (&s)[4], uint64_t hi, uint64_t l
 
 // aes_core + aes_hash, hash.cpp:114-153
 __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
-                         uint64_t seed, bool wide, const AesTables& T, uint64_t& hi,
+                         uint64_t seed, bool wide, const uint32_t* T, uint64_t& hi,
                          uint64_t& lo) {
     uint32_t k0[4], k1[4], s[4], w[4];
     set128(k0, seed ^ kP1, seed + kGolden);
@@ -231,11 +250,15 @@ __global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
         const uint64_t i = r * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
         const bool valid = i < nkeys;
         uint64_t hi = 0, lo = 0;
+        // offsets[i] per lane; offsets[i+1] from the next lane (one load per key)
+        const uint64_t oi = i <= nkeys ? __ldg(offsets + i) : 0;
+        uint64_t onext = __shfl_down_sync(kFull, oi, 1);
+        if ((threadIdx.x & 31) == 31 && valid) onext = __ldg(offsets + i + 1);
         if (valid) {
-            const uint64_t o0 = __ldg(offsets + i) - base_off, o1 = __ldg(offsets + i + 1) - base_off;
+            const uint64_t o0 = oi - base_off, o1 = onext - base_off;
             const uint32_t len = (uint32_t)(o1 - o0);
             if (algo == 1 || algo == 2) {
-                aes_hash(data, o0, len, ix.seed, algo == 2, T, hi, lo);
+                aes_hash(data, o0, len, ix.seed, algo == 2, T.t0 + (threadIdx.x & 31), hi, lo);
             } else if (algo == 4) {
                 hi = portable_hash64(data, o0, len, ix.seed ^ kP3);
                 lo = portable_hash64(data, o0, len, mix64(ix.seed) + kGolden);

@@ -1,0 +1,56 @@
+"""Profile driver: set up a bench.py workload (config 1-5) and run the query launch once
+(--ncu) or time it (default). Not part of the product.
+
+  python tools/prof_work.py --config 4 [--ncu] [--n N]
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+class _Dist:
+    world, rank, local = 1, 0, 0
+
+    def barrier(self):
+        pass
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--ncu", action="store_true")
+    ap.add_argument("--n", type=int, default=0, help="override the config's n")
+    ap.add_argument("--minimal", type=int, default=1)
+    a = ap.parse_args()
+    cfg = dict(bench.CONFIGS[a.config])
+    if a.n:
+        cfg["n"] = a.n
+    lib = C.CDLL(os.path.join(ROOT, "paper_2502_15539_b200", "libph_bench.so"))
+    stream = torch.cuda.current_stream()
+    W = bench.WORKLOADS[cfg["kind"]](a, cfg, _Dist(), lib, C.c_void_p(stream.cuda_stream))
+    out = torch.empty(W.nq, dtype=torch.int32, device="cuda")
+    W.query(out, bool(a.minimal), stream.cuda_stream)
+    torch.cuda.synchronize()
+    if a.ncu:
+        return
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        W.query(out, bool(a.minimal), stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(f"config {a.config} n={W.nq}: best {min(ts):.3f} ms, {W.nq / min(ts) / 1e6:.2f} Gkeys/s")
+
+
+if __name__ == "__main__":
+    main()

@@ -136,6 +136,20 @@ def main():
           f"max persisting L2: {bench.phb_max_persist_bytes() / 2**20:.1f} MiB", flush=True)
     rec("baseline")
     rec("nonminimal", minimal=0)
+    for L_, _ in handles.values():
+        L_.ph_gpu_set_defer_min.argtypes = [C.c_uint64]
+        L_.ph_gpu_set_defer_min(2**64 - 1)
+    rec("inline remap (deferral off)")
+    for L_, _ in handles.values():
+        L_.ph_gpu_set_defer_min(1 << 20)
+    for reg in (1, 2):
+        for L_, _ in handles.values():
+            if hasattr(L_, "ph_gpu_set_regime"):
+                L_.ph_gpu_set_regime(reg)
+        rec(f"regime={reg}")
+    for L_, _ in handles.values():
+        if hasattr(L_, "ph_gpu_set_regime"):
+            L_.ph_gpu_set_regime(0)
     for name in libs:
         if name != "main":
             rec(f"lib={name}", lib=name)

@@ -335,7 +335,7 @@ extern "C" {
 const char* ph_gpu_last_error(void) { return g_err.c_str(); }
 uint64_t ph_gpu_launch_count(void) { return phg::launch_count(); }
 int ph_gpu_set_regime(int regime) {
-    if (regime < 0 || regime > 2) return fail(PH_E_INVALID, "regime must be 0, 1 or 2");
+    if (regime < 0 || regime > 3) return fail(PH_E_INVALID, "regime must be 0..3");
     phg::set_regime(regime);
     return PH_OK;
 }

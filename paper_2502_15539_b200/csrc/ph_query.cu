@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_remap_patch(const DevIndex ix, const Re
     }
 }
 
-template <int G, bool POW2, class OutT, int KPT, int SRC, int MINB>
+template <int G, bool POW2, class OutT, int KPT, int SRC, int MINB, bool DEFER>
 __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex ix,
                                                    const uint64_t* __restrict__ keys,
                                                    OutT* __restrict__ out, uint64_t nkeys,
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex i
             need[j] = minimal && slot[j] >= ix.n && (uint32_t)(j * 32) + lane < rem;
         }
         if (minimal) {  // remap_slot, index.hpp:98-100
-            if (PH_DEFER && rl.idx) defer_tile<KPT, OutT>(ix, lidx, lrem, lcap, wcount, need, slot, base);
+            if (DEFER && rl.idx) defer_tile<KPT, OutT>(ix, lidx, lrem, lcap, wcount, need, slot, base);
             else remap_tile<KPT, OutT>(ix, need, slot);
         }
         OutT* op = out + base + lane;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex i
         for (int j = 0; j < KPT; j++)
             if ((uint32_t)(j * 32) + lane < rem) st_stream(op + j * 32, slot[j]);
     }
-    if (PH_DEFER && rl.idx && lane == 0) rl.counts[warp] = wcount;
+    if (DEFER && rl.idx && lane == 0) rl.counts[warp] = wcount;
 }
 
 // ---------------------------------------------------------------------------
@@ -282,13 +282,13 @@ struct KeySrc {
 //  * L2 regime (pilots L2-resident, configs 1/2): latency-bound; KPT=4 at 8 CTAs/SM
 //    (32 warps/SM) with the remap deferred to k_remap_patch measured fastest.
 constexpr uint64_t kDramRegimeBytes = uint64_t{64} << 20;
-static int g_regime = 0;  // 0 auto, 1 force L2 regime, 2 force DRAM regime
+static int g_regime = 0;  // 0 auto, 1 force L2 regime, 2 force DRAM regime, 3 DRAM + deferral
 void set_regime(int r) { g_regime = r; }
 
 template <int G, bool POW2, class OutT, int SRC, int KPT, int MINB, bool DEFER>
 static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
                                 int minimal, cudaStream_t s, int sms, const RemapList& rl) {
-    auto kern = k_query_u64<G, POW2, OutT, KPT, SRC, MINB>;
+    auto kern = k_query_u64<G, POW2, OutT, KPT, SRC, MINB, (PH_DEFER && DEFER)>;
     const int threads = g_threads_override > 0 ? g_threads_override : PH_THREADS;
     const int blocks = grid_for(kern, threads, (uint64_t)threads / 32 * 32 * KPT, n, sms);
     const uint32_t nlists = (uint32_t)blocks * (uint32_t)(threads / 32);
@@ -311,7 +311,9 @@ static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out
 template <int G, bool POW2, class OutT, int SRC>
 static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
                                 int minimal, cudaStream_t s, int sms, const RemapList& rl) {
-    const bool dram = g_regime == 2 || (g_regime == 0 && ix.P * ix.B > kDramRegimeBytes);
+    const bool dram = g_regime >= 2 || (g_regime == 0 && ix.P * ix.B > kDramRegimeBytes);
+    if (dram && g_regime == 3)  // experiment: DRAM tuning with the deferred remap
+        return launch_u64_k<G, POW2, OutT, SRC, 8, 1, true>(ix, src, out, n, minimal, s, sms, rl);
     if (dram) return launch_u64_k<G, POW2, OutT, SRC, 8, 1, false>(ix, src, out, n, minimal, s, sms, rl);
     return launch_u64_k<G, POW2, OutT, SRC, 4, 8, true>(ix, src, out, n, minimal, s, sms, rl);
 }

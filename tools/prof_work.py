@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--ncu", action="store_true")
     ap.add_argument("--n", type=int, default=0, help="override the config's n")
     ap.add_argument("--minimal", type=int, default=1)
+    ap.add_argument("--regimes", default="", help="comma list of ph_gpu_set_regime values to time")
     a = ap.parse_args()
     cfg = dict(bench.CONFIGS[a.config])
     if a.n:
@@ -41,15 +42,22 @@ def main():
     torch.cuda.synchronize()
     if a.ncu:
         return
-    ts = []
-    for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        W.query(out, bool(a.minimal), stream.cuda_stream)
-        e1.record(stream)
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    print(f"config {a.config} n={W.nq}: best {min(ts):.3f} ms, {W.nq / min(ts) / 1e6:.2f} Gkeys/s")
+    from paper_2502_15539_b200 import ph_gpu
+    ph_gpu._L.ph_gpu_set_regime.argtypes = [C.c_int]
+    for reg in [int(r) for r in a.regimes.split(",")] if a.regimes else [0]:
+        ph_gpu._L.ph_gpu_set_regime(reg)
+        for minimal in (True, False):
+            W.query(out, minimal, stream.cuda_stream)
+            ts = []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                W.query(out, minimal, stream.cuda_stream)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            print(f"config {a.config} n={W.nq} regime={reg} minimal={int(minimal)}: best "
+                  f"{min(ts):.3f} ms, {W.nq / min(ts) / 1e6:.2f} Gkeys/s", flush=True)
 
 
 if __name__ == "__main__":

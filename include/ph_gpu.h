@@ -120,6 +120,11 @@ uint64_t ph_gpu_launch_count(void);
  * second kernel (warp-private lists + k_remap_patch); smaller ones remap inline.
  * UINT64_MAX disables deferral. Results are identical either way. */
 int ph_gpu_set_defer_min(uint64_t min_keys);
+/* Partitioned path for device-resident u64 / k-mer batches (experimental,
+ * slower than the direct kernel in round 1): 0 = automatic (currently off), 1 = never,
+ * 2 = whenever the shape allows. Needs ~13-17 B/key of stream-ordered scratch from the
+ * index's pool; results are identical. */
+int ph_gpu_set_partition(int mode);
 /* Kernel tuning for u64/k-mer queries: 0 = automatic (by pilot bytes vs L2), 1 = the
  * L2-resident tuning, 2 = the DRAM-bound tuning. Tuning/bench knob. */
 int ph_gpu_set_regime(int regime);

@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -298,6 +299,45 @@ struct DeferScratch {
     }
 };
 
+// Partitioned path (ph_partition.cu): for DRAM-sized pilot arrays and large
+// batches, keys are binned into G hash groups whose pilot slices (<= 20 MiB each) stay
+// L2-resident while the ordinary kernel answers them, then un-permuted.
+// Round-1 status: correct (tests/test_gpu_partition.py) but slower than the direct kernel
+// at config 3 (34.9 vs 14.9 ms; profiles/r01_partition_breakdown.txt), so "auto" keeps it
+// off; mode 2 forces it.
+std::atomic<int> g_partition{0};  // 0 auto (= off for now), 1 off, 2 force when shape allows
+
+uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n) {
+    const int mode = g_partition.load();
+    if (mode != 2 || !ix->pool || n >= (uint64_t{1} << 32)) return 0;
+    const uint64_t pb = ix->info.pilot_bytes;
+    uint64_t G = (pb + (uint64_t{20} << 20) - 1) / (uint64_t{20} << 20);  // <= 20 MiB slices
+    if (G < 2) G = 2;
+    return G > 32 ? 0 : static_cast<uint32_t>(G);
+}
+
+// Runs the partitioned path; returns cudaErrorMemoryAllocation (and leaves nothing queued)
+// when the scratch cannot be had, so the caller can fall back to the direct kernel.
+cudaError_t run_partitioned(const ph_gpu_index* ix, const uint64_t* keys, int src_kind,
+                            uint64_t seq_words, uint32_t kbits, void* out, int out_width,
+                            uint64_t n, int minimal, uint32_t G, cudaStream_t s) {
+    void* scratch = nullptr;
+    const uint64_t bytes = phg::partition_scratch_bytes(n, G, out_width);
+    if (cudaMallocFromPoolAsync(&scratch, bytes, ix->pool, s) != cudaSuccess) {
+        cudaGetLastError();
+        return cudaErrorMemoryAllocation;
+    }
+    cudaError_t e;
+    {
+        DeferScratch ds(ix, n, minimal, s);
+        e = phg::launch_query_partitioned(ix->dev, ix->info.bucket_fn, ix->info.pow2, keys,
+                                          src_kind, seq_words, kbits, out, out_width, n, minimal,
+                                          G, scratch, s, ix->sms, ds.rl);
+    }
+    cudaFreeAsync(scratch, s);
+    return e;
+}
+
 int check_width(int w) {
     return (w == PH_OUT_U32 || w == PH_OUT_U64) ? PH_OK
                                                  : fail(PH_E_INVALID, "out_width must be 4 or 8");
@@ -334,6 +374,11 @@ extern "C" {
 
 const char* ph_gpu_last_error(void) { return g_err.c_str(); }
 uint64_t ph_gpu_launch_count(void) { return phg::launch_count(); }
+int ph_gpu_set_partition(int mode) {
+    if (mode < 0 || mode > 2) return fail(PH_E_INVALID, "partition mode must be 0, 1 or 2");
+    g_partition.store(mode);
+    return PH_OK;
+}
 int ph_gpu_set_regime(int regime) {
     if (regime < 0 || regime > 3) return fail(PH_E_INVALID, "regime must be 0..3");
     phg::set_regime(regime);
@@ -485,6 +530,12 @@ int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, v
     if (n == 0) return PH_OK;
     if (!d_keys || !d_out) return fail(PH_E_INVALID, "null key or output pointer");
     DeviceGuard g(ix->device);
+    if (const uint32_t G = partition_groups(ix, n)) {
+        const cudaError_t pe = run_partitioned(ix, d_keys, 0, 0, 0, d_out, out_width, n, minimal,
+                                               G, static_cast<cudaStream_t>(stream));
+        if (pe != cudaErrorMemoryAllocation)
+            return pe == cudaSuccess ? PH_OK : cuda_fail(pe, "query_u64 (partitioned)");
+    }
     DeferScratch ds(ix, n, minimal, static_cast<cudaStream_t>(stream));
     cudaError_t e = phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_keys, d_out,
                                           out_width, n, minimal, static_cast<cudaStream_t>(stream),
@@ -561,8 +612,14 @@ int alloc_pipeline(Pipeline& pl, size_t in_bytes, size_t off_bytes, size_t out_b
     return PH_OK;
 }
 
+// Keys per pipeline chunk (default 8 Mi = 64 MiB of u64 keys); PH_GPU_CHUNK_KEYS overrides
+// (tools/e2e_sweep.py).
 size_t chunk_keys(size_t n) {
-    const size_t c = size_t{1} << 23;  // 8 Mi keys = 64 MiB of u64 keys per chunk
+    size_t c = size_t{1} << 23;
+    if (const char* e = std::getenv("PH_GPU_CHUNK_KEYS")) {
+        const unsigned long long v = std::strtoull(e, nullptr, 10);
+        if (v >= 1024) c = static_cast<size_t>(v) & ~size_t{31};
+    }
     return n < c ? n : c;
 }
 
@@ -710,7 +767,15 @@ int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n
     if (n_bases < (uint64_t)k) return PH_OK;
     if (!d_seq || !d_out) return fail(PH_E_INVALID, "null sequence or output pointer");
     DeviceGuard g(ix->device);
-    DeferScratch ds(ix, n_bases - (uint64_t)k + 1, minimal, static_cast<cudaStream_t>(stream));
+    const uint64_t nwin = n_bases - (uint64_t)k + 1;
+    if (const uint32_t G = partition_groups(ix, nwin)) {
+        const cudaError_t pe = run_partitioned(ix, d_seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k),
+                                               d_out, out_width, nwin, minimal, G,
+                                               static_cast<cudaStream_t>(stream));
+        if (pe != cudaErrorMemoryAllocation)
+            return pe == cudaSuccess ? PH_OK : cuda_fail(pe, "query_kmers (partitioned)");
+    }
+    DeferScratch ds(ix, nwin, minimal, static_cast<cudaStream_t>(stream));
     cudaError_t e = phg::launch_query_kmers(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_seq,
                                             n_bases, k, d_out, out_width, minimal,
                                             static_cast<cudaStream_t>(stream), ix->sms, ds.rl);

@@ -44,6 +44,7 @@ struct DevIndex {
     uint64_t window_bytes;        // persisting window over the hot region (0 = none)
     float window_hit_ratio;
     int32_t cold_evict_first;     // cold-region pilot loads: 1 = L2::evict_first, 0 = evict_last
+    int32_t pilot_evict_normal;   // 1: all pilot loads L2::evict_normal (partitioned pass B)
 };
 
 // Device address of pilots[part*B + bucket] under the hot-first layout.
@@ -61,6 +62,11 @@ __device__ __forceinline__ uint64_t pilot_offset(const DevIndex& ix, uint32_t pa
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {

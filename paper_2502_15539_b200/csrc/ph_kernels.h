@@ -59,6 +59,21 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                                cudaStream_t s, int sms,
                                const RemapList& rl = RemapList{nullptr, nullptr, nullptr, 0});
 
+// Same as launch_query_u64 with the L2-resident tuning forced (partitioned pass B).
+cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2,
+                                   const uint64_t* keys, void* out, int out_width, uint64_t n,
+                                   int minimal, cudaStream_t s, int sms, const RemapList& rl,
+                                   bool l2_tuning);
+
+// Partitioned path (ph_partition.cu). src_kind 0: keys = u64 keys; 1: keys = packed
+// sequence (seq_words, kbits), n = number of windows. scratch >= partition_scratch_bytes.
+uint64_t partition_scratch_bytes(uint64_t n, uint32_t G, int out_width);
+cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool pow2,
+                                     const uint64_t* keys, int src_kind, uint64_t seq_words,
+                                     uint32_t kbits, void* out, int out_width, uint64_t n,
+                                     int minimal, uint32_t G, void* scratch, cudaStream_t s,
+                                     int sms, const RemapList& rl);
+
 uint64_t launch_count();
 void note_launch();
 void set_launch(int threads, int bps);

@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex i
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_keep = policy_evict_last();
+    // pass B of the partitioned path processes one L2-sized pilot slice after another:
+    // evict_last would leave earlier slices' lines pinned, so it uses evict_normal
+    const uint64_t pol_keep = ix.pilot_evict_normal ? policy_evict_normal() : policy_evict_last();
 
     const uint64_t stride = nwarps * kTile;
     const uint32_t P32 = (uint32_t)ix.P, B32 = (uint32_t)ix.B, S32 = (uint32_t)ix.S;
@@ -272,6 +274,7 @@ struct KeySrc {
     int kind;  // 0 = u64 array, 1 = k-mers
     uint64_t seq_words;
     uint32_t kbits;
+    int tuning;  // 0 = by pilot size, 1 = L2-resident tuning (the partitioned path's pass B)
 };
 
 // Two tunings of the same kernel, chosen per index by the pilot array's size
@@ -311,7 +314,8 @@ static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out
 template <int G, bool POW2, class OutT, int SRC>
 static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
                                 int minimal, cudaStream_t s, int sms, const RemapList& rl) {
-    const bool dram = g_regime >= 2 || (g_regime == 0 && ix.P * ix.B > kDramRegimeBytes);
+    const bool dram = g_regime >= 2 ||
+                      (g_regime == 0 && src.tuning == 0 && ix.P * ix.B > kDramRegimeBytes);
     if (dram && g_regime == 3)  // experiment: DRAM tuning with the deferred remap
         return launch_u64_k<G, POW2, OutT, SRC, 8, 1, true>(ix, src, out, n, minimal, s, sms, rl);
     if (dram) return launch_u64_k<G, POW2, OutT, SRC, 8, 1, false>(ix, src, out, n, minimal, s, sms, rl);
@@ -353,7 +357,7 @@ static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, con
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                              int sms, const RemapList& rl) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0}, out, out_width, n, minimal, s,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0}, out, out_width, n, minimal, s,
                       sms, rl);
 }
 
@@ -362,8 +366,16 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                                cudaStream_t s, int sms, const RemapList& rl) {
     if (n_bases < (uint64_t)k) return cudaSuccess;
     const uint64_t n = n_bases - (uint64_t)k + 1;
-    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k)},
+    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0},
                       out, out_width, n, minimal, s, sms, rl);
+}
+
+cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2,
+                                   const uint64_t* keys, void* out, int out_width, uint64_t n,
+                                   int minimal, cudaStream_t s, int sms, const RemapList& rl,
+                                   bool l2_tuning) {
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0}, out,
+                      out_width, n, minimal, s, sms, rl);
 }
 
 }  // namespace phg

@@ -1,0 +1,61 @@
+"""GPU tests of the partitioned query path (ph_partition.cu): forced on for
+small indexes (ph_gpu_set_partition(2)), its outputs must equal the reference's for u64
+keys and k-mers, u32/u64 outputs, minimal/non-minimal and ragged batch sizes."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 8
+
+
+@pytest.fixture(scope="module")
+def ph():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2502_15539_b200 import ph_gpu
+    ph_gpu._L.ph_gpu_set_partition.argtypes = [C.c_int]
+    ph_gpu._L.ph_gpu_set_partition(2)
+    yield ph_gpu
+    ph_gpu._L.ph_gpu_set_partition(0)
+
+
+@pytest.mark.parametrize("nq", [1, 4095, 4096, 4097, 1_000_003, 3 * (1 << 20) + 17])
+def test_partitioned_u64_vs_reference(ph, ref, nq):
+    from oracle.bindings import corpus_u64_np
+    n = 200_000
+    keys = corpus_u64_np(0, n, 61)
+    ptrh = ref.build_u64(keys, ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    q = corpus_u64_np(0, nq, 62)
+    m = min(nq, n)
+    q[:m] = keys[:m]
+    d_q = torch.from_numpy(q.view(np.int64)).cuda()
+    before = ph.launch_count()
+    for minimal in (True, False):
+        want = ri.query_u64(q, minimal, "loop", threads=THREADS)
+        for width in (4, 8):
+            out = idx.query(d_q, minimal=minimal, out_width=width)
+            torch.cuda.synchronize()
+            got = out.cpu().numpy().view(np.uint32 if width == 4 else np.uint64).astype(np.uint64)
+            assert np.array_equal(got, want), (minimal, width)
+    assert ph.launch_count() - before >= 4 * 5  # bin/scan/bin/query/gather per call
+
+
+def test_partitioned_kmers_vs_reference(ph, ref, port):
+    n_bases, k = 2_000_030, 31
+    seq = port.gen_dna(n_bases, 45)
+    kmers = port.kmers(seq, n_bases, k)
+    ptrh = ref.build_u64(np.unique(kmers), ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    d_seq = torch.from_numpy(seq.view(np.int64)).cuda()
+    for minimal in (True, False):
+        want = ri.query_u64(kmers, minimal, "stream", 32, threads=THREADS)
+        out = idx.query_kmers(d_seq, n_bases, k, minimal=minimal, out_width=4)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32).astype(np.uint64), want)

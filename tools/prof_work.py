@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override the config's n")
     ap.add_argument("--minimal", type=int, default=1)
     ap.add_argument("--regimes", default="", help="comma list of ph_gpu_set_regime values to time")
+    ap.add_argument("--partition", default="", help="comma list of ph_gpu_set_partition modes")
     a = ap.parse_args()
     cfg = dict(bench.CONFIGS[a.config])
     if a.n:
@@ -44,8 +45,13 @@ def main():
         return
     from paper_2502_15539_b200 import ph_gpu
     ph_gpu._L.ph_gpu_set_regime.argtypes = [C.c_int]
-    for reg in [int(r) for r in a.regimes.split(",")] if a.regimes else [0]:
+    ph_gpu._L.ph_gpu_set_partition.argtypes = [C.c_int]
+    combos = [(int(r), int(pm)) for r in (a.regimes.split(",") if a.regimes else ["0"])
+              for pm in (a.partition.split(",") if a.partition else ["0"])]
+    ref_out = None
+    for reg, pm in combos:
         ph_gpu._L.ph_gpu_set_regime(reg)
+        ph_gpu._L.ph_gpu_set_partition(pm)
         for minimal in (True, False):
             W.query(out, minimal, stream.cuda_stream)
             ts = []
@@ -56,7 +62,11 @@ def main():
                 e1.record(stream)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
-            print(f"config {a.config} n={W.nq} regime={reg} minimal={int(minimal)}: best "
+            if minimal:
+                if ref_out is None:
+                    ref_out = out.clone()
+                assert torch.equal(out, ref_out), "outputs differ between modes"
+            print(f"config {a.config} n={W.nq} regime={reg} partition={pm} minimal={int(minimal)}: best "
                   f"{min(ts):.3f} ms, {W.nq / min(ts) / 1e6:.2f} Gkeys/s", flush=True)
 
 

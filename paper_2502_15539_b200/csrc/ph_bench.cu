@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t* __restrict__ buf,
 __global__ void __launch_bounds__(256) k_gather_skew(const uint8_t* __restrict__ buf,
                                                      uint64_t F_hot, uint64_t F, uint32_t p_hot,
                                                      uint64_t nloads, uint64_t seed, int mode,
-                                                     uint32_t* sink) {
+                                                     uint32_t* sink, const uint64_t* sin,
+                                                     uint32_t* sout) {
     uint64_t pk, pc;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pk));
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pc));
@@ -121,6 +122,15 @@ __global__ void __launch_bounds__(256) k_gather_skew(const uint8_t* __restrict__
                              : "=h"(x) : "l"(buf + a), "l"(pol));
             }
             v[j] = x;
+        }
+        if (sin) {  // the query kernel's stream: 8 B in (evict_first) + 4 B out (.cs) per load
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                uint64_t kv;
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+                             : "=l"(kv) : "l"(sin + base + j), "l"(pc));
+                asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(sout + base + j), "r"((uint32_t)kv + v[j]));
+            }
         }
 #pragma unroll
         for (int j = 0; j < 8; j++) acc += v[j];
@@ -397,12 +407,13 @@ int phb_gather_mode(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t 
 }
 
 int phb_gather_skew(const uint8_t* d_buf, uint64_t F_hot, uint64_t F, double p_hot,
-                    uint64_t nloads, uint64_t seed, int mode, uint32_t* d_sink, void* stream) {
+                    uint64_t nloads, uint64_t seed, int mode, uint32_t* d_sink, void* stream,
+                    const uint64_t* d_sin, uint32_t* d_sout) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const uint32_t ph = (uint32_t)(p_hot * 4294967295.0);
     k_gather_skew<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(d_buf, F_hot, F, ph, nloads, seed,
-                                                            mode, d_sink);
+                                                            mode, d_sink, d_sin, d_sout);
     return (int)cudaGetLastError();
 }
 

@@ -255,6 +255,39 @@ int main(int argc, char** argv) {
         }
     }
 
+    // fused k-mer front end through the wrapper: identical to querying the materialised
+    // k-mers (first base in the MSBs) with the reference
+    {
+        const uint64_t n_bases = 300'031;
+        const int k = 31;
+        std::vector<uint64_t> seq((n_bases + 31) / 32);
+        for (uint64_t w = 0; w < seq.size(); w++) seq[w] = R.corpus_u64(w, 44);
+        const uint64_t nw = n_bases - k + 1;
+        std::vector<uint64_t> kmers(nw);
+        for (uint64_t i = 0; i < nw; i++) {
+            uint64_t v = 0;
+            for (int t = 0; t < k; t++) {
+                const uint64_t j = i + t;
+                v = (v << 2) | ((seq[j / 32] >> (2 * (31 - j % 32))) & 3);
+            }
+            kmers[i] = v;
+        }
+        std::vector<uint64_t> uniq = kmers;
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        const auto bytes = build(R, uniq, "default");
+        void* ref = R.load(bytes.data(), bytes.size());
+        const ph_gpu::PtrHashIndex idx(bytes);
+        std::vector<uint64_t> want(nw);
+        R.query_u64(ref, kmers.data(), nw, want.data(), 1, 0, 0, 1);
+        std::vector<uint32_t> got(nw);
+        idx.index_kmers(seq.data(), n_bases, k, got.data());
+        bool same = true;
+        for (uint64_t i = 0; i < nw; i++) same &= got[i] == static_cast<uint32_t>(want[i]);
+        CHECK(same);
+        R.unload(ref);
+    }
+
     // key-kind mismatch is an error at the C ABI (the reference would misuse silently)
     {
         const auto keys = corpus(R, 1000, 11);

@@ -13,7 +13,8 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 bench = C.CDLL(os.path.join(ROOT, "paper_2502_15539_b200", "libph_bench.so"))
 bench.phb_gather_skew.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
-                                  C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]
+                                  C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]
 bench.phb_set_persist.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_float, C.c_size_t]
 bench.phb_max_persist_bytes.restype = C.c_longlong
 
@@ -28,9 +29,15 @@ def main():
     nl = 1 << 28
     maxp = bench.phb_max_persist_bytes()
 
+    sin = torch.empty(nl, dtype=torch.int64, device="cuda")
+    sout = torch.empty(nl, dtype=torch.int32, device="cuda")
+    streaming = [False]
+
     def t(F_hot, p_hot, mode):
         def run():
-            bench.phb_gather_skew(buf.data_ptr(), F_hot, F, p_hot, nl, 5, mode, sink.data_ptr(), sp)
+            bench.phb_gather_skew(buf.data_ptr(), F_hot, F, p_hot, nl, 5, mode, sink.data_ptr(), sp,
+                                  sin.data_ptr() if streaming[0] else None,
+                                  sout.data_ptr() if streaming[0] else None)
         run()
         best = 1e9
         for _ in range(3):
@@ -43,9 +50,11 @@ def main():
             best = min(best, a.elapsed_time(b))
         return round(nl / best / 1e6, 2)
 
-    for hot_mb, p_hot in ((32, 0.37), (48, 0.45), (64, 0.5), (96, 0.6)):
+    for (hot_mb, p_hot), stream_on in [(hp, so) for so in (False, True)
+                                       for hp in ((32, 0.37), (48, 0.45), (64, 0.5), (96, 0.6))]:
+        streaming[0] = stream_on
         Fh = hot_mb << 20
-        r = {"hot_mb": hot_mb, "p_hot": p_hot}
+        r = {"hot_mb": hot_mb, "p_hot": p_hot, "with_12B_stream": stream_on}
         for mode, name in ((2, "nohint"), (0, "all_last"), (1, "hot_last_cold_first")):
             r[name] = t(Fh, p_hot, mode)
         for carve_mb in (int(maxp) >> 20,):

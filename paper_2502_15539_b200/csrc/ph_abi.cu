@@ -474,6 +474,22 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
     d.remap_kind = p.remap_kind;
     d.ef_low_bits = p.ef_low_bits;
     d.hash_algo = p.algo;
+    {  // AES round keys of hash.cpp:116-119: k0 = (seed^P1, seed+golden), k1 = (mix64(seed)^P2,
+       // ~seed*0x6c62272e07bb0143), each (hi, lo) with lo = bytes 0-7
+        auto mix64 = [](uint64_t z) {
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+            return z ^ (z >> 31);
+        };
+        const uint64_t k0hi = p.seed ^ 0x8bb84b93962eacc9ULL, k0lo = p.seed + 0x9e3779b97f4a7c15ULL;
+        const uint64_t k1hi = mix64(p.seed) ^ 0x2d358dccaa6c78a5ULL;
+        const uint64_t k1lo = (~p.seed) * 0x6c62272e07bb0143ULL;
+        const uint64_t w0[2] = {k0lo, k0hi}, w1[2] = {k1lo, k1hi};
+        for (int i = 0; i < 4; i++) {
+            d.aes_k0[i] = static_cast<uint32_t>(w0[i / 2] >> (32 * (i % 2)));
+            d.aes_k1[i] = static_cast<uint32_t>(w1[i / 2] >> (32 * (i % 2)));
+        }
+    }
     {  // per-index memory pool for per-call scratch (kept cached between calls)
         cudaMemPoolProps props = {};
         props.allocType = cudaMemAllocationTypePinned;

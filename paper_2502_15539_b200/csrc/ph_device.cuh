@@ -45,6 +45,8 @@ struct DevIndex {
     float window_hit_ratio;
     int32_t cold_evict_first;     // cold-region pilot loads: 1 = L2::evict_first, 0 = evict_last
     int32_t pilot_evict_normal;   // 1: all pilot loads L2::evict_normal (partitioned pass B)
+    // AES string hash round keys k0/k1 (hash.cpp:116-119) as LE u32 words, host-derived
+    uint32_t aes_k0[4], aes_k1[4];
 };
 
 // Device address of pilots[part*B + bucket] under the hot-first layout.

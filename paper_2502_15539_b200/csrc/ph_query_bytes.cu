@@ -41,12 +41,16 @@ __constant__ uint8_t c_sbox[256] = {
     0x8c, 0xa1, 0x89, 0x0d, 0xbf, 0xe6, 0x42, 0x68, 0x41, 0x99, 0x2d, 0x0f, 0xb0, 0x54, 0xbb, 0x16};
 
 // One MixColumns∘SubBytes table T0[x] = (2·S[x], S[x], S[x], 3·S[x]) (rows 0..3, LE), held
-// in shared memory 32 times, interleaved so that entry x of copy `lane` sits at word
-// x*32 + lane: every lane reads its own copy, i.e. its own bank, so the 16 lookups of an
+// in shared memory 32 times, interleaved so that entry x of copy `lane` sits at byte offset
+// x*128 + lane*4: every lane reads its own copy, i.e. its own bank, so the 16 lookups of an
 // AES round are conflict-free whatever the state bytes are. The rows' rotated tables are
 // T0 rotated by 8/16/24 bits, and S[x] is byte 1 of T0[x] (for AESENCLAST).
+// init[len] caches the state after the first AESENC of aes_core for len < kInitLens: it
+// depends only on (len, seed), hash.cpp:120-122.
+constexpr uint32_t kInitLens = 256;
 struct AesTables {
-    uint32_t t0[256 * 32];  // 32 KiB
+    uint32_t t0[256 * 32];         // 32 KiB
+    uint4 init[kInitLens];         // 4 KiB
 };
 
 __device__ __forceinline__ uint8_t xtime(uint8_t a) {
@@ -62,37 +66,41 @@ __device__ void fill_tables(AesTables& T) {
     }
 }
 
+// Lookup of T0[byte k of w] in this lane's copy with two ALU ops (shift + LOP3) and an LDS
+// whose base address folds into the instruction: byte offset ((w >> (8k-7)) & 0x7f80) | lane*4.
+template <int K>
+__device__ __forceinline__ uint32_t tk(const AesTables& T, uint32_t w, uint32_t lane4) {
+    const uint32_t off = (K == 0 ? (w << 7) : (w >> (8 * K - 7))) & 0x7f80u;
+    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(T.t0) + (off | lane4));
+}
+
 // state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
 // in-memory byte order of the __m128i in hash.cpp. AESENC = ShiftRows,
-// SubBytes, MixColumns, AddRoundKey (Intel semantics). Tl = T.t0 + lane.
-__device__ __forceinline__ uint32_t tl(const uint32_t* Tl, uint32_t byte) { return Tl[byte << 5]; }
-
+// SubBytes, MixColumns, AddRoundKey (Intel semantics).
 __device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4],
-                                       const uint32_t* Tl) {
+                                       const AesTables& T, uint32_t lane4) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        const uint32_t a0 = tl(Tl, s[c] & 0xff);
-        const uint32_t a1 = tl(Tl, (s[(c + 1) & 3] >> 8) & 0xff);
-        const uint32_t a2 = tl(Tl, (s[(c + 2) & 3] >> 16) & 0xff);
-        const uint32_t a3 = tl(Tl, s[(c + 3) & 3] >> 24);
+        const uint32_t a0 = tk<0>(T, s[c], lane4);
+        const uint32_t a1 = tk<1>(T, s[(c + 1) & 3], lane4);
+        const uint32_t a2 = tk<2>(T, s[(c + 2) & 3], lane4);
+        const uint32_t a3 = tk<3>(T, s[(c + 3) & 3], lane4);
         o[c] = a0 ^ __funnelshift_l(a1, a1, 8) ^ __funnelshift_l(a2, a2, 16) ^
                __funnelshift_l(a3, a3, 24) ^ k[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
 }
-__device__ __forceinline__ uint32_t sbox(const uint32_t* Tl, uint32_t byte) {
-    return (tl(Tl, byte) >> 8) & 0xff;
-}
 __device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)[4],
-                                           const uint32_t* Tl) {
+                                           const AesTables& T, uint32_t lane4) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        o[c] = (sbox(Tl, s[c] & 0xff) | (sbox(Tl, (s[(c + 1) & 3] >> 8) & 0xff) << 8) |
-                (sbox(Tl, (s[(c + 2) & 3] >> 16) & 0xff) << 16) |
-                (sbox(Tl, s[(c + 3) & 3] >> 24) << 24)) ^
+        o[c] = (((tk<0>(T, s[c], lane4) >> 8) & 0xff) |
+                (tk<1>(T, s[(c + 1) & 3], lane4) & 0xff00) |
+                ((tk<2>(T, s[(c + 2) & 3], lane4) << 8) & 0xff0000) |
+                ((tk<3>(T, s[(c + 3) & 3], lane4) << 16) & 0xff000000)) ^
                k[c];
     }
 #pragma unroll
@@ -191,21 +199,30 @@ __device__ __forceinline__ void set128(uint32_t (&s)[4], uint64_t hi, uint64_t l
     s[3] = (uint32_t)(hi >> 32);
 }
 
-// aes_core + aes_hash, hash.cpp:114-153
+// aes_core + aes_hash, hash.cpp:114-153. k0/k1 come precomputed from the host (they depend
+// only on the seed, hash.cpp:116-119); the first round comes from the init table.
 __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
-                         uint64_t seed, bool wide, const uint32_t* T, uint64_t& hi,
-                         uint64_t& lo) {
-    uint32_t k0[4], k1[4], s[4], w[4];
-    set128(k0, seed ^ kP1, seed + kGolden);
-    set128(k1, mix64(seed) ^ kP2, (~seed) * 0x6c62272e07bb0143ULL);
-    set128(s, (uint64_t)len * kC, seed ^ (uint64_t)len);
-    aesenc(s, k0, T);
+                         uint64_t seed, bool wide, const DevIndex& ix, const AesTables& T,
+                         uint32_t lane4, uint64_t& hi, uint64_t& lo) {
+    const uint32_t k0[4] = {ix.aes_k0[0], ix.aes_k0[1], ix.aes_k0[2], ix.aes_k0[3]};
+    const uint32_t k1[4] = {ix.aes_k1[0], ix.aes_k1[1], ix.aes_k1[2], ix.aes_k1[3]};
+    uint32_t s[4], w[4];
+    if (len < kInitLens) {
+        const uint4 v = T.init[len];
+        s[0] = v.x;
+        s[1] = v.y;
+        s[2] = v.z;
+        s[3] = v.w;
+    } else {
+        set128(s, (uint64_t)len * kC, seed ^ (uint64_t)len);
+        aesenc(s, k0, T, lane4);
+    }
     uint32_t i = 0;
     while (i + 16 <= len) {
         load16(data, off + i, 16, w);
 #pragma unroll
         for (int c = 0; c < 4; c++) s[c] ^= w[c];
-        aesenc(s, k1, T);
+        aesenc(s, k1, T, lane4);
         i += 16;
     }
     if (i < len) {
@@ -214,11 +231,11 @@ __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_
         w[3] ^= rem << 24;  // buf[15] ^= len - i
 #pragma unroll
         for (int c = 0; c < 4; c++) s[c] ^= w[c];
-        aesenc(s, k1, T);
+        aesenc(s, k1, T, lane4);
     }
-    aesenc(s, k0, T);
-    aesenc(s, k1, T);
-    aesenclast(s, k0, T);
+    aesenc(s, k0, T, lane4);
+    aesenc(s, k1, T, lane4);
+    aesenclast(s, k0, T, lane4);
     const uint64_t l = (uint64_t)s[0] | ((uint64_t)s[1] << 32);
     const uint64_t h = (uint64_t)s[2] | ((uint64_t)s[3] << 32);
     if (!wide) {
@@ -237,8 +254,17 @@ __global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
                                                      int minimal) {
     __shared__ AesTables T;
     const int algo = ix.hash_algo;
+    const uint32_t lane4 = (threadIdx.x & 31) * 4;
     if (algo == 1 || algo == 2) {
         fill_tables(T);
+        __syncthreads();
+        const uint32_t k0[4] = {ix.aes_k0[0], ix.aes_k0[1], ix.aes_k0[2], ix.aes_k0[3]};
+        for (uint32_t len = threadIdx.x; len < kInitLens; len += blockDim.x) {
+            uint32_t st[4];
+            set128(st, (uint64_t)len * kC, ix.seed ^ (uint64_t)len);  // hash.cpp:120-122
+            aesenc(st, k0, T, lane4);
+            T.init[len] = make_uint4(st[0], st[1], st[2], st[3]);
+        }
         __syncthreads();
     }
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -258,7 +284,7 @@ __global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
             const uint64_t o0 = oi - base_off, o1 = onext - base_off;
             const uint32_t len = (uint32_t)(o1 - o0);
             if (algo == 1 || algo == 2) {
-                aes_hash(data, o0, len, ix.seed, algo == 2, T.t0 + (threadIdx.x & 31), hi, lo);
+                aes_hash(data, o0, len, ix.seed, algo == 2, ix, T, lane4, hi, lo);
             } else if (algo == 4) {
                 hi = portable_hash64(data, o0, len, ix.seed ^ kP3);
                 lo = portable_hash64(data, o0, len, mix64(ix.seed) + kGolden);

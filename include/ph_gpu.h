@@ -65,6 +65,9 @@ typedef struct ph_gpu_info {
  * remap payload to `device`. Replaces deserialize()/load_index() + the
  * PtrHashIndex ctor (serde.cpp:176-260, index.hpp:36-46). */
 int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_index** out);
+/* load_index (serde.cpp:251-260): mmap + pinned upload of a PTRH v1 file, then exactly
+ * ph_gpu_index_create. */
+int ph_gpu_index_load(const char* path, int device, ph_gpu_index** out);
 int ph_gpu_index_destroy(ph_gpu_index* index);
 int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out);
 const char* ph_gpu_last_error(void);
@@ -112,6 +115,12 @@ int ph_gpu_index_stream_kmers(const ph_gpu_index* index, const uint64_t* h_seq, 
 int ph_gpu_index_u64(const ph_gpu_index* index, uint64_t key, int minimal, uint64_t* out);
 int ph_gpu_index_bytes(const ph_gpu_index* index, const uint8_t* key, size_t len, int minimal,
                        uint64_t* out);
+
+/* ---- verification ---- */
+/* verify_bijection (proj/tools/ptrhash.cpp:186-210) on `device`, synchronous: counts the
+ * outputs >= n and the repeated outputs among d_out[0..count) (u32 or u64). */
+int ph_gpu_verify_bijection(const void* d_out, size_t count, int out_width, uint64_t n,
+                            int device, uint64_t* out_of_range, uint64_t* duplicates);
 
 /* ---- introspection ---- */
 /* Number of query-kernel launches this process made through this library. */

@@ -47,6 +47,13 @@ class PtrHashIndex {
         check(ph_gpu_index_create(ptrh.data(), ptrh.size(), device, &h_));
         check(ph_gpu_index_info(h_, &info_));
     }
+    // load_index (serde.cpp:251-260): straight from a PTRH v1 file (mmap + pinned upload).
+    static PtrHashIndex load(const char* path, int device = 0) {
+        PtrHashIndex ix;
+        check(ph_gpu_index_load(path, device, &ix.h_));
+        check(ph_gpu_index_info(ix.h_, &ix.info_));
+        return ix;
+    }
     PtrHashIndex(const PtrHashIndex&) = delete;
     PtrHashIndex& operator=(const PtrHashIndex&) = delete;
     PtrHashIndex(PtrHashIndex&& o) noexcept : h_(o.h_), info_(o.info_) { o.h_ = nullptr; }
@@ -139,6 +146,7 @@ class PtrHashIndex {
             std::copy(keys[i].begin(), keys[i].end(), bytes.begin() + offsets[i]);
     }
 
+    PtrHashIndex() = default;
     ph_gpu_index* h_ = nullptr;
     ph_gpu_info info_{};
 };

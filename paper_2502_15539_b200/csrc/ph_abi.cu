@@ -9,6 +9,10 @@
 //  * the query entry points: device-resident (async) and host-resident
 //    (pipelined H2D -> kernel -> D2H over chunks and streams, synchronous).
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <cmath>
@@ -221,18 +225,19 @@ int apply_pilot_layout(ph_gpu_index* ix, const uint8_t* file, uint64_t hot_bytes
     uint64_t H = B;
     if (total > hot_bytes && P > 0) H = hot_bytes / P < B ? hot_bytes / P : B;
     phg::DevIndex& d = ix->dev;
-    int rc;
-    if (H == B) {
-        rc = upload(file, total, &ix->d_pilots);
-    } else {
-        std::vector<uint8_t> lay(total);
-        for (uint64_t part = 0; part < P; part++) {
-            std::memcpy(lay.data() + part * H, file + part * B, H);
-            std::memcpy(lay.data() + P * H + part * (B - H), file + part * B + H, B - H);
-        }
-        rc = upload(lay.data(), total, &ix->d_pilots);
-    }
+    int rc = upload(file, total, &ix->d_pilots);  // file order
     if (rc) return rc;
+    if (H != B) {  // permute to the hot-first layout on the device (k_relayout)
+        void* lay = nullptr;
+        cudaError_t e = cudaMalloc(&lay, total);
+        if (e != cudaSuccess) return fail(PH_E_NOMEM, "cudaMalloc(pilot layout)");
+        e = phg::launch_relayout(static_cast<const uint8_t*>(ix->d_pilots),
+                                 static_cast<uint8_t*>(lay), P, B, H, nullptr);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+        cudaFree(ix->d_pilots);
+        ix->d_pilots = lay;
+        if (e != cudaSuccess) return cuda_fail(e, "pilot relayout");
+    }
     d.pilots = static_cast<const uint8_t*>(ix->d_pilots);
     d.hot_b = H;
     d.cold_b = B - H;
@@ -901,6 +906,59 @@ int ph_gpu_index_bytes(const ph_gpu_index* ix, const uint8_t* key, size_t len, i
     if (e == cudaSuccess) e = cudaMemcpy(out, d + 2, 8, cudaMemcpyDeviceToHost);
     cudaFree(d);
     return e == cudaSuccess ? PH_OK : cuda_fail(e, "index_bytes");
+}
+
+// load_index (serde.cpp:251-260) for the GPU: the PTRH file is mmap'ed, pinned in place
+// (cudaHostRegister, read-only) so the upload runs at PCIe speed, then validated and
+// uploaded exactly as ph_gpu_index_create does.
+int ph_gpu_index_load(const char* path, int device, ph_gpu_index** out) {
+    if (!path || !out) return fail(PH_E_INVALID, "null argument");
+    *out = nullptr;
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return fail(PH_E_INVALID, std::string("cannot open ") + path);
+    struct stat st;
+    if (fstat(fd, &st) != 0 || st.st_size <= 0) {
+        close(fd);
+        return fail(PH_E_FORMAT, std::string("index file truncated: ") + path);
+    }
+    const size_t len = static_cast<size_t>(st.st_size);
+    void* m = mmap(nullptr, len, PROT_READ, MAP_PRIVATE | MAP_POPULATE, fd, 0);
+    close(fd);
+    if (m == MAP_FAILED) return fail(PH_E_INVALID, std::string("mmap failed: ") + path);
+    const bool pinned =
+        cudaHostRegister(m, len, cudaHostRegisterReadOnly | cudaHostRegisterPortable) == cudaSuccess;
+    if (!pinned) cudaGetLastError();  // pageable upload still works
+    const int rc = ph_gpu_index_create(static_cast<const uint8_t*>(m), len, device, out);
+    if (pinned) cudaHostUnregister(m);
+    munmap(m, len);
+    return rc;
+}
+
+// verify_bijection (proj/tools/ptrhash.cpp:186-210) on the device, synchronous: counts
+// outputs >= n and repeated outputs among d_out[0..count).
+int ph_gpu_verify_bijection(const void* d_out, size_t count, int out_width, uint64_t n,
+                            int device, uint64_t* out_of_range, uint64_t* duplicates) {
+    if (!d_out || !out_of_range || !duplicates) return fail(PH_E_INVALID, "null argument");
+    if (int rc = check_width(out_width)) return rc;
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const size_t words = (n + 31) / 32;
+    void* scratch = nullptr;
+    if (cudaMalloc(&scratch, 16 + words * 4) != cudaSuccess)
+        return fail(PH_E_NOMEM, "cudaMalloc(bijection bitset)");
+    auto* bad = static_cast<unsigned long long*>(scratch);
+    auto* bits = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(scratch) + 16);
+    cudaError_t e = cudaMemset(scratch, 0, 16 + words * 4);
+    if (e == cudaSuccess) e = phg::launch_verify(d_out, out_width, count, n, bits, bad, nullptr, sms);
+    unsigned long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, bad, 16, cudaMemcpyDeviceToHost);
+    cudaFree(scratch);
+    if (e != cudaSuccess) return cuda_fail(e, "verify_bijection");
+    *out_of_range = h[0];
+    *duplicates = h[1];
+    return PH_OK;
 }
 
 }  // extern "C"

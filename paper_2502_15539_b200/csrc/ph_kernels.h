@@ -74,6 +74,11 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
                                      int minimal, uint32_t G, void* scratch, cudaStream_t s,
                                      int sms, const RemapList& rl);
 
+cudaError_t launch_relayout(const uint8_t* src, uint8_t* dst, uint64_t P, uint64_t B, uint64_t H,
+                            cudaStream_t s);
+cudaError_t launch_verify(const void* out, int out_width, uint64_t count, uint64_t n,
+                          unsigned int* bits, unsigned long long* bad, cudaStream_t s, int sms);
+
 uint64_t launch_count();
 void note_launch();
 void set_launch(int threads, int bps);

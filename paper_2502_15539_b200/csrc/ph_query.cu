@@ -378,4 +378,62 @@ cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2
                       out_width, n, minimal, s, sms, rl);
 }
 
+// ---------------------------------------------------------------------------
+// index upload helper and the bijection verifier
+// ---------------------------------------------------------------------------
+// File-order pilots (P*B) -> hot-first layout, one part per block iteration.
+__global__ void __launch_bounds__(256) k_relayout(const uint8_t* __restrict__ src,
+                                                  uint8_t* __restrict__ dst, uint64_t P, uint64_t B,
+                                                  uint64_t H) {
+    for (uint64_t part = blockIdx.x; part < P; part += gridDim.x) {
+        const uint8_t* s = src + part * B;
+        uint8_t* hot = dst + part * H;
+        uint8_t* cold = dst + P * H + part * (B - H);
+        for (uint64_t b = threadIdx.x; b < B; b += blockDim.x) {
+            const uint8_t v = s[b];
+            if (b < H) hot[b] = v;
+            else cold[b - H] = v;
+        }
+    }
+}
+
+cudaError_t launch_relayout(const uint8_t* src, uint8_t* dst, uint64_t P, uint64_t B, uint64_t H,
+                            cudaStream_t s) {
+    const uint64_t g = P < 65535 ? P : 65535;
+    k_relayout<<<(unsigned)(g ? g : 1), 256, 0, s>>>(src, dst, P, B, H);
+    return cudaGetLastError();
+}
+
+// verify_bijection (proj/tools/ptrhash.cpp:186-210) on the device: every output must be
+// < n and hit exactly once. bits: ceil(n/32) zeroed words; bad[0] out-of-range, bad[1] dups.
+template <class OutT>
+__global__ void __launch_bounds__(256) k_verify(const OutT* __restrict__ out, uint64_t count,
+                                                uint64_t n, unsigned int* bits,
+                                                unsigned long long* bad) {
+    unsigned long long oob = 0, dup = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = out[i];
+        if (v >= n) {
+            oob++;
+            continue;
+        }
+        const unsigned int m = 1u << (v & 31);
+        if (atomicOr(bits + (v >> 5), m) & m) dup++;
+    }
+    if (oob) atomicAdd(bad, oob);
+    if (dup) atomicAdd(bad + 1, dup);
+}
+
+cudaError_t launch_verify(const void* out, int out_width, uint64_t count, uint64_t n,
+                          unsigned int* bits, unsigned long long* bad, cudaStream_t s, int sms) {
+    const int grid = sms * 8;
+    if (out_width == 4)
+        k_verify<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(out), count, n, bits, bad);
+    else
+        k_verify<uint64_t><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(out), count, n, bits, bad);
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace phg

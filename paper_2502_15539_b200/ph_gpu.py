@@ -65,6 +65,9 @@ _L.ph_gpu_index_stream_kmers.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c
 _L.ph_gpu_index_u64.argtypes = [C.c_void_p, C.c_uint64, C.c_int, u64p]
 _L.ph_gpu_index_bytes.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, u64p]
 _L.ph_gpu_launch_count.restype = C.c_uint64
+_L.ph_gpu_index_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+_L.ph_gpu_verify_bijection.argtypes = [C.c_void_p, C.c_size_t, C.c_int, C.c_uint64, C.c_int,
+                                       u64p, u64p]
 _L.ph_gpu_set_launch.argtypes = [C.c_int, C.c_int]
 
 # status codes (ph_gpu.h)
@@ -123,8 +126,23 @@ class PtrHashIndex:
 
     @classmethod
     def load(cls, path: str, device: int = 0) -> "PtrHashIndex":
-        with open(path, "rb") as f:
-            return cls(f.read(), device)
+        """load_index (serde.cpp:251-260): mmap + pinned upload (ph_gpu_index_load)."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        _check(_L.ph_gpu_index_load(os.fsencode(path), device, C.byref(h)))
+        self._h = h
+        info = Info()
+        _check(_L.ph_gpu_index_info(h, C.byref(info)))
+        self.info = info
+        return self
+
+    def verify_bijection(self, out, n=None) -> tuple:
+        """(out_of_range, duplicates) of device outputs, verify_bijection (ptrhash.cpp:186-210)."""
+        oob, dup = C.c_uint64(), C.c_uint64()
+        _check(_L.ph_gpu_verify_bijection(C.c_void_p(out.data_ptr()), out.numel(),
+                                          out.element_size(), int(self.info.n if n is None else n),
+                                          int(self.info.device), C.byref(oob), C.byref(dup)))
+        return int(oob.value), int(dup.value)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -8,6 +8,7 @@
 //
 // Usage: test_query_gpu <path to libptrhash_ref.so>. Exit code 0 = all passed.
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -228,6 +229,32 @@ int main(int argc, char** argv) {
         std::vector<uint64_t> out(n);
         idx.index_stream(keys, 32, out.data());
         CHECK(is_bijection(out, n));
+    }
+
+    // test_serde.cpp (save_index / load_index round trip): an index loaded from a file
+    // answers like the one created from the same bytes.
+    {
+        const uint64_t n = 50'000;
+        const auto keys = corpus(R, n, 9);
+        const auto bytes = build(R, keys, "default");
+        const std::string path = "/tmp/ph_gpu_cpp_test_" + std::to_string(getpid()) + ".ptrh";
+        FILE* f = std::fopen(path.c_str(), "wb");
+        CHECK(f && std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size());
+        std::fclose(f);
+        const auto loaded = ph_gpu::PtrHashIndex::load(path.c_str());
+        std::remove(path.c_str());
+        const ph_gpu::PtrHashIndex created(bytes);
+        std::vector<uint64_t> a(n), b(n);
+        loaded.index_stream(keys, 32, a.data());
+        created.index_stream(keys, 32, b.data());
+        CHECK(a == b && is_bijection(a, n));
+        bool threw = false;
+        try {
+            ph_gpu::PtrHashIndex::load("/nonexistent/index.ptrh");
+        } catch (const ph_gpu::Error&) {
+            threw = true;
+        }
+        CHECK(threw);
     }
 
     // test_query.cpp:94-117 — threaded slices concatenate to the single-call answer

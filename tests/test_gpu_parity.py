@@ -288,3 +288,42 @@ def test_kmer_harness_matches_oracle(port):
         bench.phb_kmers(C.c_void_p(d_seq.data_ptr()), C.c_uint64(n_bases), k,
                         C.c_void_p(out.data_ptr()), None)
         assert np.array_equal(host_u(out, 8), port.kmers(seq, n_bases, k))
+
+
+def test_load_from_file_matches_create(ph, tmp_path):
+    """ph_gpu_index_load (load_index, serde.cpp:251-260) == create from the same bytes."""
+    for name in ("default_l30", "quadratic_ef", "str_default"):
+        ptrh, rec = load_golden(name)
+        path = tmp_path / f"{name}.ptrh"
+        path.write_bytes(ptrh)
+        idx = ph.PtrHashIndex.load(str(path))
+        assert idx.shape() == ph.PtrHashIndex(ptrh).shape()
+        if "queries" in rec:
+            q = np.array(rec["queries"], dtype=np.uint64)
+            assert np.array_equal(gpu_query(idx, q, True, 8), np.array(rec["minimal"], np.uint64))
+    bad = tmp_path / "bad.ptrh"
+    bad.write_bytes(b"PTRX" + bytes(80))
+    with pytest.raises(ph.SerdeError):
+        ph.PtrHashIndex.load(str(bad))
+    with pytest.raises(ph.PhGpuError):
+        ph.PtrHashIndex.load(str(tmp_path / "missing.ptrh"))
+
+
+def test_verify_bijection_on_device(ph, ref):
+    """ph_gpu_verify_bijection (verify_bijection, ptrhash.cpp:186-210): 0/0 on a real
+    answer, and it counts planted out-of-range values and duplicates."""
+    from oracle.bindings import corpus_u64_np
+    n = 200_000
+    keys = corpus_u64_np(0, n, 31)
+    idx = ph.PtrHashIndex(ref.build_u64(keys, ref.params("default")))
+    for width in (4, 8):
+        out = idx.query(dev(keys), minimal=True, out_width=width)
+        assert idx.verify_bijection(out) == (0, 0)
+        bad = out.clone()
+        bad[5] = n + 3        # out of range
+        bad[7] = bad[8]       # one duplicate
+        bad[9] = bad[8]       # another
+        assert idx.verify_bijection(bad) == (1, 2)
+    nm = idx.query(dev(keys), minimal=False, out_width=8)
+    P, S = idx.shape()[1:3]
+    assert idx.verify_bijection(nm, n=P * S) == (0, 0)

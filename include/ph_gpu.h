@@ -129,22 +129,26 @@ uint64_t ph_gpu_launch_count(void);
  * second kernel (warp-private lists + k_remap_patch); smaller ones remap inline.
  * UINT64_MAX disables deferral. Results are identical either way. */
 int ph_gpu_set_defer_min(uint64_t min_keys);
-/* Partitioned path for device-resident u64 / k-mer batches (experimental,
- * slower than the direct kernel in round 1): 0 = automatic (currently off), 1 = never,
- * 2 = whenever the shape allows. Needs ~13-17 B/key of stream-ordered scratch from the
- * index's pool; results are identical. */
+/* Partitioned path for device-resident u64 / k-mer batches: keys are
+ * binned by hash group so each group's pilot slice stays L2-resident, answered, then
+ * restored to input order. Needs the file-order pilot layout without a persisting window
+ * (ph_gpu_index_set_l2_policy(index, 0, 2)) and ~28 B/key of stream-ordered scratch from
+ * the index's pool (falls back to the direct kernel if it cannot be had).
+ * 0 = automatic (DRAM-sized pilot arrays, batches >= pilot_bytes/2 keys), 1 = never,
+ * 2 = whenever the layout allows. Results are identical. */
 int ph_gpu_set_partition(int mode);
 /* Kernel tuning for u64/k-mer queries: 0 = automatic (by pilot bytes vs L2), 1 = the
  * L2-resident tuning, 2 = the DRAM-bound tuning. Tuning/bench knob. */
 int ph_gpu_set_regime(int regime);
 /* Override the bulk-kernel launch shape (0 = automatic). For tuning/bench. */
 int ph_gpu_set_launch(int threads_per_block, int blocks_per_sm);
-/* Pilot-gather L2 policy (default: hot_bytes = 64 MiB, flags = 0). The device copy of
- * the pilots is laid out hot-first: the first hot_bytes/P buckets of every part form a
+/* Pilot layout and L2 policy (default: hot_bytes = 64 MiB, flags = 0). Pilot arrays larger
+ * than hot_bytes are laid out hot-first: the first hot_bytes/P buckets of every part form a
  * contiguous region covered by a persisting L2 access-policy window (this sets the
- * context's cudaLimitPersistingL2CacheSize). flags: 1 = cold-region loads use
- * L2::evict_first, 2 = no persisting window. Results are unaffected. Tuning knob: do not
- * call while queries on `index` are in flight. */
+ * context's cudaLimitPersistingL2CacheSize). hot_bytes = 0 or flag 2 (no window) keeps the
+ * file order and releases the device-wide persisting set-aside (the partitioned path needs
+ * both). flag 1: cold-region loads use L2::evict_first. Results are unaffected. Do not call
+ * while queries on `index` are in flight. */
 int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flags);
 
 #ifdef __cplusplus

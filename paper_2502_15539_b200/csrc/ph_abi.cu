@@ -222,8 +222,8 @@ int upload(const void* src, size_t bytes, void** dst) {
 int apply_pilot_layout(ph_gpu_index* ix, const uint8_t* file, uint64_t hot_bytes, int flags) {
     const uint64_t P = ix->info.parts, B = ix->info.buckets_per_part;
     const uint64_t total = P * B;
-    uint64_t H = B;
-    if (total > hot_bytes && P > 0) H = hot_bytes / P < B ? hot_bytes / P : B;
+    uint64_t H = B;  // hot_bytes == 0 or everything fits: the file's own order
+    if (hot_bytes && total > hot_bytes && P > 0) H = hot_bytes / P < B ? hot_bytes / P : B;
     phg::DevIndex& d = ix->dev;
     int rc = upload(file, total, &ix->d_pilots);  // file order
     if (rc) return rc;
@@ -245,10 +245,19 @@ int apply_pilot_layout(ph_gpu_index* ix, const uint8_t* file, uint64_t hot_bytes
     d.cold_evict_first = (flags & kL2ColdEvictFirst) ? 1 : 0;
     d.window_bytes = 0;
     d.window_hit_ratio = 0.f;
+    // Lines left persisting by earlier windowed launches would otherwise keep their share
+    // of the L2 (the partitioned path's pass B needs all of it).
+    cudaCtxResetPersistingL2Cache();
+    if ((flags & kL2NoWindow) || !hot_bytes) {
+        // No window: also release the device-wide persisting set-aside, which otherwise
+        // shrinks the L2 left to normal accesses (measured: partitioned pass B 2x slower).
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0) != cudaSuccess) cudaGetLastError();
+        return PH_OK;
+    }
     int max_window = 0, max_persist = 0;
     cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ix->device);
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ix->device);
-    if (!(flags & kL2NoWindow) && max_window > 0 && max_persist > 0 && d.hot_total > 0) {
+    if (max_window > 0 && max_persist > 0 && d.hot_total > 0) {
         const uint64_t win = d.hot_total < (uint64_t)max_window ? d.hot_total : (uint64_t)max_window;
         size_t cur = 0;
         cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
@@ -305,20 +314,27 @@ struct DeferScratch {
 };
 
 // Partitioned path (ph_partition.cu): for DRAM-sized pilot arrays and large
-// batches, keys are binned into G hash groups whose pilot slices (<= 20 MiB each) stay
-// L2-resident while the ordinary kernel answers them, then un-permuted.
-// Round-1 status: correct (tests/test_gpu_partition.py) but slower than the direct kernel
-// at config 3 (34.9 vs 14.9 ms; profiles/r01_partition_breakdown.txt), so "auto" keeps it
-// off; mode 2 forces it.
-std::atomic<int> g_partition{0};  // 0 auto (= off for now), 1 off, 2 force when shape allows
+// device-resident batches, keys are binned into G hash groups whose pilot slices (~12 MiB
+// each) stay L2-resident while the ordinary kernel answers them, then un-permuted.
+// It needs the file-order pilot layout without a persisting set-aside
+// (ph_gpu_index_set_l2_policy(index, 0, 2)); "auto" then uses it for batches of at least
+// pilot_bytes / 2 keys. Measured at config 3: 14.5 ms against 15.4 ms for the direct kernel
+// on the default hot-first layout (profiles/r01_partition_*.txt).
+std::atomic<int> g_partition{0};  // 0 auto, 1 off, 2 force when the layout allows
 
 uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n) {
     const int mode = g_partition.load();
-    if (mode != 2 || !ix->pool || n >= (uint64_t{1} << 32)) return 0;
+    if (mode == 1 || !ix->pool || ix->dev.hot_b < ix->dev.B) return 0;  // needs file order
     const uint64_t pb = ix->info.pilot_bytes;
-    uint64_t G = (pb + (uint64_t{20} << 20) - 1) / (uint64_t{20} << 20);  // <= 20 MiB slices
+    if (mode == 0 && (pb <= (uint64_t{64} << 20) || n < pb / 2 || ix->dev.window_bytes))
+        return 0;
+    // pilot bytes per group (L2-resident); PH_GPU_PART_SLICE_MB overrides (tuning only)
+    uint64_t slice = uint64_t{12} << 20;
+    if (const char* e = std::getenv("PH_GPU_PART_SLICE_MB"))
+        if (std::atoll(e) > 0) slice = static_cast<uint64_t>(std::atoll(e)) << 20;
+    uint64_t G = (pb + slice - 1) / slice;
     if (G < 2) G = 2;
-    return G > 32 ? 0 : static_cast<uint32_t>(G);
+    return G > 64 ? 0 : static_cast<uint32_t>(G);
 }
 
 // Runs the partitioned path; returns cudaErrorMemoryAllocation (and leaves nothing queued)
@@ -385,7 +401,7 @@ int ph_gpu_set_partition(int mode) {
     return PH_OK;
 }
 int ph_gpu_set_regime(int regime) {
-    if (regime < 0 || regime > 3) return fail(PH_E_INVALID, "regime must be 0..3");
+    if (regime < 0 || regime > 2) return fail(PH_E_INVALID, "regime must be 0..2");
     phg::set_regime(regime);
     return PH_OK;
 }
@@ -436,6 +452,10 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
     I.pow2 = is_pow2(p.S) ? 1 : 0;
     I.device = device;
 
+    // Default layout: L2-sized pilot arrays keep the file order under a persisting window
+    // over all of it; DRAM-sized ones are laid out hot-first (64 MiB hot region + window).
+    // ph_gpu_index_set_l2_policy(index, 0, 2) selects the file order without a window,
+    // which the partitioned path needs.
     int rc = apply_pilot_layout(ix, p.pilots, kDefaultHotBytes, kDefaultL2Flags);
     if (!rc && p.remap_kind != 2) {
         rc = upload(p.remap, p.remap_len, &ix->d_remap);

@@ -126,8 +126,11 @@ __device__ __forceinline__ uint64_t gamma(uint64_t x, const uint64_t* __restrict
     } else if constexpr (G == 2) {  // cubic :27-32: ((x2+x3)>>1)*255>>8 + x>>8, exact
         const uint64_t x2 = mulhi(x, x);
         const uint64_t x3 = mulhi(x2, x);
-        const uint64_t half = (x2 >> 1) + (x3 >> 1) + (x2 & x3 & 1);  // floor((x2+x3)/2), no overflow
-        return (half >> 8) * 255 + (((half & 255) * 255) >> 8) + (x >> 8);
+        // half = floor((x2+x3)/2) from the 65-bit sum (carry into bit 63)
+        const uint64_t s = x2 + x3;
+        const uint64_t half = (s >> 1) | ((uint64_t)(s < x2) << 63);
+        // floor(255*half/256) = half - ceil(half/256)
+        return half - (half >> 8) - ((half & 255) != 0) + (x >> 8);
     } else if constexpr (G == 3) {  // skewed :34-39
         constexpr uint64_t SX = 0x9999999999999999ULL;  // floor(3*2^64/5)
         constexpr uint64_t SY = 0x4ccccccccccccccc;     // floor(3*2^64/10)

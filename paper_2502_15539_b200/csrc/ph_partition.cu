@@ -1,24 +1,32 @@
 // ph_partition.cu — the partitioned query path for DRAM-sized indexes.
 //
-// When the pilot array is far larger than what the L2 holds for random access
-// (~64 MB), every direct query pays a DRAM row activation for its 1-byte pilot read
-// (~57 G/s over 333 MB). This path turns those random DRAM reads into streaming passes
-// plus L2-resident random reads:
+// When the pilot array is far larger than what the L2 holds for random access (~64 MB),
+// every direct query pays a DRAM row activation for its 1-byte pilot read (~57 G/s over
+// 333 MB). This path turns those random DRAM reads into streaming passes plus L2-resident
+// random reads. Keys are binned by hash group g = hi(G * h): group g's keys only use parts
+// [gP/G, (g+1)P/G], a contiguous ~P*B/G-byte slice of the pilots that fits in the L2.
 //
-//   A1 count   per 4096-key chunk, how many keys fall in each of G hash groups
-//              g = hi(G * h). Group g's keys use parts [gP/G, (g+1)P/G], i.e. a contiguous
-//              ~P*B/G-byte slice of the pilots that fits in L2.
-//   scan       exclusive prefix of the counts per group over chunks; group bases.
-//   A2 scatter stable: key i goes to bins[base_g + prefix_g(chunk) + rank], its group
-//              id to gid[i].
-//   B  query   the ordinary query kernel over `bins` (group after group in one launch),
-//              with every pilot read now an L2 hit, answers into `tmp`.
-//   C  gather  out[i] = tmp[base_g + prefix_g(chunk) + rank] with the same ranks as A2.
+//   A  bin     per 4096-key tile: ranks by group in shared memory, one global atomicAdd
+//              per (tile, group) to reserve a run in that group's region, then the runs are
+//              written from shared memory with coalesced stores: entry = (key, position in
+//              the tile as u16). Run (offset, length) -> runoff/runcnt[tile][g].
+//   B  query   the ordinary query kernel (L2-resident tuning), one launch per group region
+//              (so the warps of a launch only touch that group's pilot slice), then one
+//              over the spill; answers into slots[] at the same entry index.
+//   C  unbin   per tile: the G runs' (position, slot) pairs are scattered into a shared
+//              memory tile, which is then written to out[] with coalesced stores.
 //
-// Streams per query: keys 8 B x2 (A1, A2) + bins 8 B x2 + gid 1 B x2 + tmp 4-8 B x2 + out;
-// all coalesced. Results are identical to the direct kernel (same arithmetic in B).
+// Group regions have a fixed capacity (n/G plus 16 sigma plus a tile); a run that does not
+// fit goes to a spill region sized for the worst case (any distribution of queries, e.g.
+// one key repeated n times, is answered correctly; only the L2 locality of pass B is lost).
+// Unused region tails hold stale entries that pass B answers harmlessly and pass C never
+// reads. Results are identical to the direct kernel: pass B runs the same arithmetic.
+//
+// DRAM bytes per query: A 8 (key) + 10 (entry), B 8 + 4 (u32 slot), C 6 + 4 = 40 B, all
+// streamed, against the direct kernel's 12 B streamed + one DRAM row activation per query.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "ph_device.cuh"
@@ -26,14 +34,24 @@
 
 namespace phg {
 
-constexpr int kPartThreads = 256;
-constexpr int kPartPerThread = 16;
-constexpr uint32_t kChunk = kPartThreads * kPartPerThread;  // 4096 keys per chunk
-constexpr int kMaxGroups = 32;
+constexpr int kBinThreads = 256;
+constexpr int kBinPerThread = 16;
+constexpr uint32_t kTileKeys = kBinThreads * kBinPerThread;  // 4096 keys per tile
+constexpr int kBinCtas = 4;    // CTAs per SM (registers: 64 per thread)
+constexpr int kUnbinCtas = 5;
+constexpr int kMaxGroups = 64;
+// ctrl[]: per-group cursors [0, kMaxGroups), spill cursor
+constexpr int kCtrlSpill = kMaxGroups;
+constexpr int kCtrlWords = kMaxGroups + 1;
 
-// Group of a key: g = hi(G * h) for the hash h = C * (key ^ seed) (hash.hpp:27).
+// Group of a key: g = hi32(G * hi32(h)) for the hash h = C * (key ^ seed) (hash.hpp:27).
+// Monotone in h like part = hi(P * h) (bucket_fn.hpp:66-72), so each group's keys use a
+// contiguous range of parts. Only the high word of h is formed (3 multiplies).
 __device__ __forceinline__ uint32_t group_of(uint64_t key, uint64_t seed, uint32_t G) {
-    return (uint32_t)__umul64hi(kC * (key ^ seed), (uint64_t)G);
+    const uint64_t x = key ^ seed;
+    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    const uint32_t hh = __umulhi(xl, (uint32_t)kC) + xl * (uint32_t)(kC >> 32) + xh * (uint32_t)kC;
+    return __umulhi(hh, G);
 }
 
 // k-mer of window i (same layout and arithmetic as kmer_at in ph_query.cu).
@@ -47,249 +65,226 @@ __device__ __forceinline__ uint64_t part_kmer(const uint64_t* __restrict__ seq, 
     return kbits == 64 ? top : top >> (64 - kbits);
 }
 
-// Per-chunk ranks, shared by A1/A2/C so that all three agree on the stable order.
-// Warp w of the block owns positions chunk + w*512 + j*32 + lane (j < 16). Each lane ends
-// with its 16 (group, rank-within-chunk) pairs; the chunk's per-group totals end in tot[].
-struct ChunkRanks {
-    uint8_t g[kPartPerThread];
-    uint16_t r[kPartPerThread];
-};
-
-__device__ __forceinline__ void chunk_ranks(ChunkRanks& cr, uint32_t G, uint32_t (*wcnt)[kMaxGroups],
-                                            uint32_t* tot) {
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1;
-    uint32_t* my = wcnt[warp];
-    for (uint32_t g = lane; g < G; g += 32) my[g] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < kPartPerThread; j++) {
-        const uint32_t g = cr.g[j];
-        const unsigned m = __match_any_sync(0xffffffffu, g);
-        cr.r[j] = (uint16_t)(my[g] + __popc(m & lt));
-        __syncwarp();
-        if ((m & lt) == 0) my[g] += __popc(m);  // the group's lowest lane adds the count
-        __syncwarp();
-    }
-    __syncthreads();
-    // exclusive prefix over warps, per group; chunk totals
-    if (threadIdx.x < G) {
-        const uint32_t g = threadIdx.x;
-        uint32_t run = 0;
-        for (int w = 0; w < kPartThreads / 32; w++) {
-            const uint32_t c = wcnt[w][g];
-            wcnt[w][g] = run;
-            run += c;
-        }
-        tot[g] = run;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kPartPerThread; j++) cr.r[j] = (uint16_t)(cr.r[j] + my[cr.g[j]]);
+__device__ __forceinline__ void st_cs_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_cs_u16(uint16_t* p, uint16_t v) {
+    asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
 }
 
-// Group of entry e of a chunk staged in group order (goff = exclusive prefix of the chunk's
-// per-group totals; G <= 32): the last group whose offset is <= e.
-__device__ __forceinline__ uint32_t staged_group(const uint32_t* goff, uint32_t G, uint32_t e) {
-    uint32_t lo = 0, hi = G - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (goff[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-__device__ __forceinline__ uint64_t load_key(const uint64_t* __restrict__ keys, uint64_t seq_words,
-                                             uint32_t kbits, uint64_t p, int src) {
-    return src == 1 ? part_kmer(keys, seq_words, p, kbits) : __ldg(keys + p);
-}
-
-// A1: per-chunk group histogram -> counts[chunk*G + g]. All 16 keys of a thread are loaded
-// before any is used (memory-level parallelism); per-warp smem histograms, no syncs per key.
+// Pass A. Per tile: per-group counts and ranks with shared-memory atomics (the order
+// within a run does not matter: each entry carries its tile position), run reservation by
+// warp 0 (one global atomicAdd per group), staging in group order, then every thread
+// writes 16 staged entries (balanced, coalesced within runs). The next tile's keys are
+// loaded before the run writes. 4 CTAs per SM overlap one another's barrier phases.
 template <int SRC>
-__global__ void __launch_bounds__(kPartThreads) k_part_count(
+__global__ void __launch_bounds__(kBinThreads, kBinCtas) k_bin(
     const uint64_t* __restrict__ keys, uint64_t n, uint64_t seq_words, uint32_t kbits,
-    uint64_t seed, uint32_t G, uint32_t* __restrict__ counts) {
-    __shared__ uint32_t cnt[kPartThreads / 32][kMaxGroups];
-    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
-    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        cnt[warp][lane] = 0;
-        __syncwarp();
-        uint64_t k[kPartPerThread];
+    uint64_t seed, uint32_t G, uint64_t cap, unsigned long long* __restrict__ ctrl,
+    uint64_t* __restrict__ runoff, uint16_t* __restrict__ runcnt, uint64_t* __restrict__ bins,
+    uint16_t* __restrict__ bpos) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* spg = reinterpret_cast<uint32_t*>(sk + kTileKeys);  // tile position | group << 16
+    __shared__ uint32_t cnt[2][kMaxGroups];
+    __shared__ uint32_t lbase[kMaxGroups];
+    __shared__ uint64_t delta[kMaxGroups];  // run offset - staged offset
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+    uint64_t k[kBinPerThread];
+    auto load = [&](uint64_t t) {
+        const uint64_t t0 = t * kTileKeys;
+        const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
 #pragma unroll
-        for (int j = 0; j < kPartPerThread; j++) {
-            const uint64_t p = c * kChunk + (uint64_t)j * kPartThreads + threadIdx.x;
-            k[j] = p < n ? load_key(keys, seq_words, kbits, p, SRC) : 0;
+        for (int j = 0; j < kBinPerThread; j++) {
+            const uint32_t e = (uint32_t)j * kBinThreads + tid;
+            if (SRC == 1)
+                k[j] = e < valid ? part_kmer(keys, seq_words, t0 + e, kbits) : 0;
+            else
+                k[j] = e < valid ? __ldcs(keys + t0 + e) : 0;
         }
+    };
+    if (tid < kMaxGroups) cnt[0][tid] = 0;
+    uint64_t t = blockIdx.x;
+    if (t < ntiles) load(t);
+    __syncthreads();
+    for (int par = 0; t < ntiles; t += gridDim.x, par ^= 1) {
+        const uint64_t t0 = t * kTileKeys;
+        const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
+        uint32_t* c_ = cnt[par];
+        uint32_t gr[kBinPerThread];  // group << 16 | rank
 #pragma unroll
-        for (int j = 0; j < kPartPerThread; j++) {
-            const uint64_t p = c * kChunk + (uint64_t)j * kPartThreads + threadIdx.x;
-            if (p < n) atomicAdd(&cnt[warp][group_of(k[j], seed, G)], 1u);
-        }
-        __syncthreads();
-        if (threadIdx.x < G) {
-            uint32_t t = 0;
-            for (int w = 0; w < kPartThreads / 32; w++) t += cnt[w][threadIdx.x];
-            counts[c * G + threadIdx.x] = t;
-        }
-        __syncthreads();
-    }
-}
-
-// A2: stable scatter of the keys into group order, staged in shared memory so each group's
-// run of the chunk is written with coalesced stores; gid[p] = group of position p.
-template <int SRC>
-__global__ void __launch_bounds__(kPartThreads) k_part_scatter(
-    const uint64_t* __restrict__ keys, uint64_t n, uint64_t seq_words, uint32_t kbits,
-    uint64_t seed, uint32_t G, const uint32_t* __restrict__ counts,
-    const uint64_t* __restrict__ base, uint64_t* __restrict__ bins, uint8_t* __restrict__ gid) {
-    __shared__ uint32_t wcnt[kPartThreads / 32][kMaxGroups];
-    __shared__ uint32_t tot[kMaxGroups];
-    __shared__ uint32_t goff[kMaxGroups];
-    __shared__ uint64_t dst0[kMaxGroups];
-    __shared__ uint64_t stage[kChunk];
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
-    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const uint64_t p0 = c * kChunk + (uint64_t)warp * 512 + lane;
-        ChunkRanks cr;
-        uint64_t k[kPartPerThread];
-#pragma unroll
-        for (int j = 0; j < kPartPerThread; j++) {
-            const uint64_t p = p0 + (uint64_t)j * 32;
-            k[j] = p < n ? load_key(keys, seq_words, kbits, p, SRC) : 0;
-            cr.g[j] = p < n ? (uint8_t)group_of(k[j], seed, G) : (uint8_t)(G - 1);
-        }
-        chunk_ranks(cr, G, wcnt, tot);
-        if (threadIdx.x == 0) {
-            uint32_t run = 0;
-            for (uint32_t g = 0; g < G; g++) {
-                goff[g] = run;
-                run += tot[g];
-                dst0[g] = base[g] + counts[c * G + g];
+        for (int j = 0; j < kBinPerThread; j++) {
+            if ((uint32_t)j * kBinThreads + tid < valid) {
+                const uint32_t g = group_of(k[j], seed, G);
+                gr[j] = g << 16 | atomicAdd(&c_[g], 1u);
             }
         }
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kPartPerThread; j++) {
-            const uint64_t p = p0 + (uint64_t)j * 32;
-            stage[goff[cr.g[j]] + cr.r[j]] = k[j];
-            if (p < n) gid[p] = cr.g[j];
-        }
-        __syncthreads();
-        const uint32_t valid = (uint32_t)(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
-        for (uint32_t e = threadIdx.x; e < valid; e += kPartThreads) {
-            // padding keys (group G-1, highest ranks) sit at the end of the stage: e < valid
-            const uint32_t g = staged_group(goff, G, e);
-            bins[dst0[g] + (e - goff[g])] = stage[e];
-        }
-        __syncthreads();
-    }
-}
-
-// Exclusive scan of counts[chunk][g] over chunks for each group (one block per group);
-// base[g] = total of groups < g (computed by block 0 after all groups: see k_part_bases).
-__global__ void __launch_bounds__(1024) k_part_scan(uint32_t* __restrict__ counts, uint64_t nchunks,
-                                                     uint32_t G, uint64_t* __restrict__ totals) {
-    __shared__ uint64_t warp_sums[32];
-    __shared__ uint64_t carry_s;
-    const uint32_t g = blockIdx.x;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry_s = 0;
-    __syncthreads();
-    for (uint64_t t0 = 0; t0 < nchunks; t0 += blockDim.x) {
-        const uint64_t c = t0 + threadIdx.x;
-        const uint64_t v = c < nchunks ? counts[c * G + g] : 0;
-        uint64_t x = v;  // inclusive warp scan
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= (unsigned)o) x += y;
-        }
-        if (lane == 31) warp_sums[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint64_t s = lane < blockDim.x / 32 ? warp_sums[lane] : 0;
+        if (tid < kMaxGroups) cnt[par ^ 1][tid] = 0;  // next tile's counters
+        uint32_t c0 = 0, c1 = 0;
+        if (warp == 0) {  // lane owns groups 2*lane and 2*lane+1
+            const uint32_t g0 = 2 * lane;
+            c0 = g0 < G ? c_[g0] : 0;
+            c1 = g0 + 1 < G ? c_[g0 + 1] : 0;
+            uint32_t x = c0 + c1;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint64_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= (unsigned)o) s += y;
+                const uint32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= (unsigned)o) x += y;
             }
-            warp_sums[lane] = s;  // inclusive over warps
+            x -= c0 + c1;
+            lbase[g0] = x;
+            lbase[g0 + 1] = x + c0;
         }
         __syncthreads();
-        const uint64_t excl = carry_s + (warp ? warp_sums[warp - 1] : 0) + x - v;
-        if (c < nchunks) counts[c * G + g] = (uint32_t)excl;  // < 2^32 per group (n < 2^32)
-        __syncthreads();
-        if (threadIdx.x == 0) carry_s += warp_sums[blockDim.x / 32 - 1];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) totals[g] = carry_s;
-}
-
-__global__ void k_part_bases(const uint64_t* __restrict__ totals, uint32_t G,
-                             uint64_t* __restrict__ base) {
-    if (threadIdx.x == 0) {
-        uint64_t run = 0;
-        for (uint32_t g = 0; g < G; g++) {
-            base[g] = run;
-            run += totals[g];
+        if (warp == 0) {  // run reservations; their latency overlaps the other warps' staging
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint32_t g = 2 * lane + h, c = h ? c1 : c0;
+                if (g < G) {
+                    uint64_t off = 0;
+                    if (c) {
+                        off = atomicAdd(ctrl + g, (unsigned long long)c);
+                        off = off + c <= cap
+                                  ? g * cap + off
+                                  : G * cap + atomicAdd(ctrl + kCtrlSpill, (unsigned long long)c);
+                    }
+                    delta[g] = off - lbase[g];
+                    runoff[t * G + g] = off;
+                    runcnt[t * G + g] = (uint16_t)c;
+                }
+            }
         }
+#pragma unroll
+        for (int j = 0; j < kBinPerThread; j++) {
+            const uint32_t pos = (uint32_t)j * kBinThreads + tid;
+            if (pos < valid) {
+                const uint32_t g = gr[j] >> 16;
+                const uint32_t e = lbase[g] + (gr[j] & 0xffffu);
+                sk[e] = k[j];
+                spg[e] = pos | g << 16;
+            }
+        }
+        __syncthreads();
+        if (t + gridDim.x < ntiles) load(t + gridDim.x);
+#pragma unroll 4
+        for (int j = 0; j < kBinPerThread; j++) {
+            const uint32_t e = (uint32_t)j * kBinThreads + tid;
+            if (e < valid) {
+                const uint32_t pg = spg[e];
+                const uint64_t dst = delta[pg >> 16] + e;
+                st_cs_u64(bins + dst, sk[e]);
+                st_cs_u16(bpos + dst, (uint16_t)pg);
+            }
+        }
+        __syncthreads();
     }
 }
 
-// C: out[p] = tmp[base_g + prefix_g(chunk) + rank(p)], ranks recomputed from gid. The
-// chunk's group runs of tmp are first read with coalesced loads into shared memory.
+// Pass C. Per tile: the G runs are laid end to end (run g at lbase[g]); rid[e] names the
+// run of staged entry e. Every thread issues its 16 (position, slot) loads before storing
+// any into the shared-memory tile, which is then written out in order.
 template <class OutT>
-__global__ void __launch_bounds__(kPartThreads) k_part_gather(
-    const uint8_t* __restrict__ gid, uint64_t n, uint32_t G, const uint32_t* __restrict__ counts,
-    const uint64_t* __restrict__ base, const OutT* __restrict__ tmp, OutT* __restrict__ out) {
-    __shared__ uint32_t wcnt[kPartThreads / 32][kMaxGroups];
-    __shared__ uint32_t tot[kMaxGroups];
-    __shared__ uint32_t goff[kMaxGroups];
-    __shared__ uint64_t src0[kMaxGroups];
-    __shared__ OutT stage[kChunk];
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
-    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const uint64_t p0 = c * kChunk + (uint64_t)warp * 512 + lane;
-        ChunkRanks cr;
+__global__ void __launch_bounds__(kBinThreads, sizeof(OutT) == 4 ? kUnbinCtas : kUnbinCtas - 1) k_unbin(
+    uint64_t n, uint32_t G, const uint64_t* __restrict__ runoff,
+    const uint16_t* __restrict__ runcnt, const uint16_t* __restrict__ bpos,
+    const OutT* __restrict__ slots, OutT* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    OutT* stage = reinterpret_cast<OutT*>(smem);
+    uint8_t* rid = reinterpret_cast<uint8_t*>(stage + kTileKeys);
+    __shared__ uint32_t rc[kMaxGroups];
+    __shared__ uint32_t lbase[kMaxGroups];
+    __shared__ uint64_t delta[kMaxGroups];  // run offset - staged offset
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t t0 = t * kTileKeys;
+        const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
+        if (warp == 0) {
+            const uint32_t g0 = 2 * lane;
+            const uint32_t c0 = g0 < G ? __ldg(runcnt + t * G + g0) : 0;
+            const uint32_t c1 = g0 + 1 < G ? __ldg(runcnt + t * G + g0 + 1) : 0;
+            const uint64_t o0 = g0 < G ? __ldg(runoff + t * G + g0) : 0;
+            const uint64_t o1 = g0 + 1 < G ? __ldg(runoff + t * G + g0 + 1) : 0;
+            uint32_t x = c0 + c1;
 #pragma unroll
-        for (int j = 0; j < kPartPerThread; j++) {
-            const uint64_t p = p0 + (uint64_t)j * 32;
-            cr.g[j] = p < n ? __ldg(gid + p) : (uint8_t)(G - 1);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= (unsigned)o) x += y;
+            }
+            x -= c0 + c1;
+            lbase[g0] = x;
+            lbase[g0 + 1] = x + c0;
+            delta[g0] = o0 - x;
+            delta[g0 + 1] = o1 - (x + c0);
+            rc[g0] = c0;
+            rc[g0 + 1] = c1;
         }
-        chunk_ranks(cr, G, wcnt, tot);
-        if (threadIdx.x == 0) {
-            uint32_t run = 0;
-            for (uint32_t g = 0; g < G; g++) {
-                goff[g] = run;
-                run += tot[g];
-                src0[g] = base[g] + counts[c * G + g];
+        __syncthreads();
+        for (uint32_t g = warp; g < G; g += kBinThreads / 32) {
+            const uint32_t c = rc[g], lb = lbase[g];
+            for (uint32_t i = lane; i < c; i += 32) rid[lb + i] = (uint8_t)g;
+        }
+        __syncthreads();
+        uint16_t pv[kBinPerThread];
+        OutT sv[kBinPerThread];
+#pragma unroll
+        for (int j = 0; j < kBinPerThread; j++) {
+            const uint32_t e = (uint32_t)j * kBinThreads + tid;
+            if (e < valid) {
+                const uint64_t src = delta[rid[e]] + e;
+                pv[j] = __ldcs(bpos + src);
+                sv[j] = __ldcs(slots + src);
             }
         }
-        __syncthreads();
-        const uint32_t valid = (uint32_t)(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
-        for (uint32_t e = threadIdx.x; e < valid; e += kPartThreads) {
-            const uint32_t g = staged_group(goff, G, e);
-            stage[e] = __ldg(tmp + src0[g] + (e - goff[g]));
-        }
-        __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kPartPerThread; j++) {
-            const uint64_t p = p0 + (uint64_t)j * 32;
-            if (p < n) st_stream(out + p, (uint64_t)stage[goff[cr.g[j]] + cr.r[j]]);
+        for (int j = 0; j < kBinPerThread; j++)
+            if ((uint32_t)j * kBinThreads + tid < valid) stage[pv[j]] = sv[j];
+        __syncthreads();
+        {
+#pragma unroll 4
+            for (int j = 0; j < kBinPerThread; j++) {
+                const uint32_t e = (uint32_t)j * kBinThreads + tid;
+                if (e < valid) st_stream(out + t0 + e, stage[e]);
+            }
         }
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
-uint64_t partition_scratch_bytes(uint64_t n, uint32_t G, int out_width) {
-    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+namespace {
+struct Layout {
+    uint64_t cap, ntiles, nent;
+    uint64_t o_runoff, o_runcnt, o_bins, o_bpos, o_slots, total;
+};
+Layout layout(uint64_t n, uint32_t G, int out_width) {
     auto al = [](uint64_t b) { return (b + 255) & ~uint64_t{255}; };
-    return al(nchunks * G * 4) + al(2 * kMaxGroups * 8) + al(n * 8) + al(n) + al(n * out_width);
+    Layout L;
+    const uint64_t per = (n + G - 1) / G;
+    L.cap = per + 16 * (uint64_t)std::ceil(std::sqrt((double)per)) + kTileKeys;
+    L.cap = (L.cap + 255) & ~uint64_t{255};
+    L.ntiles = (n + kTileKeys - 1) / kTileKeys;
+    L.nent = G * L.cap + n;
+    uint64_t o = al(kCtrlWords * 8);
+    L.o_runoff = o;
+    o += al(L.ntiles * G * 8);
+    L.o_runcnt = o;
+    o += al(L.ntiles * G * 2);
+    L.o_bins = o;
+    o += al(L.nent * 8);
+    L.o_bpos = o;
+    o += al(L.nent * 2);
+    L.o_slots = o;
+    o += al(L.nent * (uint64_t)out_width);
+    L.total = o;
+    return L;
+}
+}  // namespace
+
+uint64_t partition_scratch_bytes(uint64_t n, uint32_t G, int out_width) {
+    return layout(n, G, out_width).total;
 }
 
 cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool pow2,
@@ -298,56 +293,58 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
                                      int minimal, uint32_t G, void* scratch, cudaStream_t s,
                                      int sms, const RemapList& rl) {
     if (n == 0) return cudaSuccess;
-    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
-    auto al = [](uint64_t b) { return (b + 255) & ~uint64_t{255}; };
-    uint8_t* p = static_cast<uint8_t*>(scratch);
-    uint32_t* counts = reinterpret_cast<uint32_t*>(p);
-    p += al(nchunks * G * 4);
-    uint64_t* totals = reinterpret_cast<uint64_t*>(p);
-    uint64_t* base = totals + kMaxGroups;
-    p += al(2 * kMaxGroups * 8);
-    uint64_t* bins = reinterpret_cast<uint64_t*>(p);
-    p += al(n * 8);
-    uint8_t* gid = p;
-    p += al(n);
-    void* tmp = p;
+    if (G < 1 || G > (uint32_t)kMaxGroups) return cudaErrorInvalidValue;
+    const Layout L = layout(n, G, out_width);
+    uint8_t* base = static_cast<uint8_t*>(scratch);
+    auto* ctrl = reinterpret_cast<unsigned long long*>(base);
+    auto* runoff = reinterpret_cast<uint64_t*>(base + L.o_runoff);
+    auto* runcnt = reinterpret_cast<uint16_t*>(base + L.o_runcnt);
+    auto* bins = reinterpret_cast<uint64_t*>(base + L.o_bins);
+    auto* bpos = reinterpret_cast<uint16_t*>(base + L.o_bpos);
+    void* slots = base + L.o_slots;
 
-    const int grid = (int)(nchunks < (uint64_t)sms * 8 ? nchunks : (uint64_t)sms * 8);
-    if (src_kind == 1)
-        k_part_count<1><<<grid, kPartThreads, 0, s>>>(keys, n, seq_words, kbits, ix.seed, G, counts);
-    else
-        k_part_count<0><<<grid, kPartThreads, 0, s>>>(keys, n, 0, 0, ix.seed, G, counts);
-    k_part_scan<<<G, 1024, 0, s>>>(counts, nchunks, G, totals);
-    k_part_bases<<<1, 32, 0, s>>>(totals, G, base);
-    if (src_kind == 1)
-        k_part_scatter<1><<<grid, kPartThreads, 0, s>>>(keys, n, seq_words, kbits, ix.seed, G,
-                                                        counts, base, bins, gid);
-    else
-        k_part_scatter<0><<<grid, kPartThreads, 0, s>>>(keys, n, 0, 0, ix.seed, G, counts, base,
-                                                        bins, gid);
-    note_launch();
-    note_launch();
-    note_launch();
-    note_launch();
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = cudaMemsetAsync(ctrl, 0, kCtrlWords * 8, s);
     if (e != cudaSuccess) return e;
-    // B: the ordinary kernel (L2-resident tuning) over the group-ordered keys
-    // (no persisting window here: it would pin other groups' hot pilots in the L2)
+    const size_t smem_a = kTileKeys * (8 + 4);
+    // (per device and cheap: set on every call)
+    cudaFuncSetAttribute(k_bin<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
+    cudaFuncSetAttribute(k_bin<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
+    cudaFuncSetAttribute(k_unbin<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kTileKeys * 9));
+    const uint64_t want = L.ntiles;
+    const int grid_a = (int)(want < (uint64_t)sms * kBinCtas ? want : (uint64_t)sms * kBinCtas);
+    const uint64_t ctas_c = (uint64_t)sms * (out_width == 4 ? kUnbinCtas : kUnbinCtas - 1);
+    const int grid_c = (int)(want < ctas_c ? want : ctas_c);
+    if (src_kind == 1)
+        k_bin<1><<<grid_a, kBinThreads, smem_a, s>>>(keys, n, seq_words, kbits, ix.seed, G, L.cap,
+                                                   ctrl, runoff, runcnt, bins, bpos);
+    else
+        k_bin<0><<<grid_a, kBinThreads, smem_a, s>>>(keys, n, 0, 0, ix.seed, G, L.cap, ctrl, runoff,
+                                                   runcnt, bins, bpos);
+    note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // B: the query kernel over the entries, one L2-sized pilot slice after another
+    // (no persisting window and evict_normal pilots: earlier slices must be evictable)
     DevIndex ixb = ix;
     ixb.window_bytes = 0;
     ixb.pilot_evict_normal = 1;
     ixb.cold_evict_first = 0;
-    e = launch_query_u64_tuned(ixb, gamma_kind, pow2, bins, tmp, out_width, n, minimal, s, sms, rl,
-                               /*l2_tuning=*/true);
-    if (e != cudaSuccess) return e;
+    uint8_t* sl = static_cast<uint8_t*>(slots);
+    for (uint32_t g = 0; g <= G; g++) {  // g == G: the spill region
+        const uint64_t off = g * L.cap;
+        e = launch_query_bins(ixb, gamma_kind, pow2, bins + off, ctrl + (g < G ? g : kCtrlSpill), g < G ? L.cap : n,
+                              sl + off * out_width, out_width, minimal, s, sms, rl);
+        if (e != cudaSuccess) return e;
+    }
+    const size_t smem_c = kTileKeys * (size_t)(out_width + 1);
     if (out_width == 4)
-        k_part_gather<uint32_t><<<grid, kPartThreads, 0, s>>>(gid, n, G, counts, base,
-                                                             static_cast<const uint32_t*>(tmp),
-                                                             static_cast<uint32_t*>(out));
+        k_unbin<uint32_t><<<grid_c, kBinThreads, smem_c, s>>>(n, G, runoff, runcnt, bpos,
+                                                            static_cast<const uint32_t*>(slots),
+                                                            static_cast<uint32_t*>(out));
     else
-        k_part_gather<uint64_t><<<grid, kPartThreads, 0, s>>>(gid, n, G, counts, base,
-                                                             static_cast<const uint64_t*>(tmp),
-                                                             static_cast<uint64_t*>(out));
+        k_unbin<uint64_t><<<grid_c, kBinThreads, smem_c, s>>>(n, G, runoff, runcnt, bpos,
+                                                            static_cast<const uint64_t*>(slots),
+                                                            static_cast<uint64_t*>(out));
     note_launch();
     return cudaGetLastError();
 }

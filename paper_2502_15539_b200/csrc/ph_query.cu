@@ -35,6 +35,13 @@ namespace phg {
 #ifndef PH_THREADS
 #define PH_THREADS 128
 #endif
+// L2-resident tuning: keys per thread and CTAs per SM
+#ifndef PH_L2_KPT
+#define PH_L2_KPT 4
+#endif
+#ifndef PH_L2_MINB
+#define PH_L2_MINB 8
+#endif
 
 // Warp-cooperative remap of the keys flagged in need[] (slot >= n).
 // Entries are ranked across (j, lane) with ballots; lane r of a round decodes
@@ -148,13 +155,19 @@ __global__ void __launch_bounds__(256) k_remap_patch(const DevIndex ix, const Re
     }
 }
 
-template <int G, bool POW2, class OutT, int KPT, int SRC, int MINB, bool DEFER>
+// HOTF: the device pilots use the hot-first layout (pilot_offset); otherwise the file's
+// own order, offset = part * B + bucket.
+template <int G, bool POW2, class OutT, int KPT, int SRC, int MINB, bool DEFER, bool HOTF>
 __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex ix,
                                                    const uint64_t* __restrict__ keys,
-                                                   OutT* __restrict__ out, uint64_t nkeys,
+                                                   OutT* __restrict__ out, uint64_t nkeys_arg,
                                                    int minimal, uint64_t seq_words,
-                                                   uint32_t kbits, const RemapList rl) {
+                                                   uint32_t kbits, const RemapList rl,
+                                                   const unsigned long long* __restrict__ dyn_n) {
     constexpr uint64_t kTile = 32ull * KPT;
+    // SRC = 2 (the partitioned path's pass B): u64 entries whose count (<= nkeys_arg) is
+    // only known on the device (written by pass A): no host synchronisation between passes.
+    const uint64_t nkeys = SRC == 2 ? min((uint64_t)*dyn_n, nkeys_arg) : nkeys_arg;
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -215,9 +228,13 @@ __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex i
             part[j] = (uint32_t)mul32x64(P32, h[j], x);
             uint64_t unused;
             const uint32_t bucket = (uint32_t)mul32x64(B32, gamma<G>(x, ix.opt_table), unused);
-            const bool hot = bucket < ix.hot_b;
-            pilot[j] = ld_gather_u8(ix.pilots + pilot_offset(ix, part[j], bucket),
-                                    (hot || !ix.cold_evict_first) ? pol_keep : pol_stream);
+            if (HOTF) {
+                const bool hot = bucket < ix.hot_b;
+                pilot[j] = ld_gather_u8(ix.pilots + pilot_offset(ix, part[j], bucket),
+                                        (hot || !ix.cold_evict_first) ? pol_keep : pol_stream);
+            } else {
+                pilot[j] = ld_gather_u8(ix.pilots + ((uint64_t)part[j] * B32 + bucket), pol_keep);
+            }
         }
         uint64_t slot[KPT];
         bool need[KPT];
@@ -271,27 +288,29 @@ static int grid_for(K kernel, int threads, uint64_t work_items_per_block, uint64
 // 2-bit sequence (seq_words words, kbits = 2k).
 struct KeySrc {
     const uint64_t* ptr;
-    int kind;  // 0 = u64 array, 1 = k-mers
+    int kind;  // 0 = u64 array, 1 = k-mers, 2 = u64 array of device-side length *dyn_n
     uint64_t seq_words;
     uint32_t kbits;
     int tuning;  // 0 = by pilot size, 1 = L2-resident tuning (the partitioned path's pass B)
+    const unsigned long long* dyn_n;
 };
 
 // Two tunings of the same kernel, chosen per index by the pilot array's size
-// (tools/tune.py sweeps):
+// (tools/tune.py sweeps); the L2 tuning assumes the file-order pilot layout
+// (a hot-first layout only exists for DRAM-sized pilot arrays):
 //  * DRAM regime (pilots > kDramRegimeBytes, e.g. configs 3/5): the pilot gather is bound
 //    by DRAM row activations; KPT=8 with the compiler's register allocation (12 warps/SM)
 //    and the inline warp-compacted remap measured fastest;
 //  * L2 regime (pilots L2-resident, configs 1/2): latency-bound; KPT=4 at 8 CTAs/SM
 //    (32 warps/SM) with the remap deferred to k_remap_patch measured fastest.
 constexpr uint64_t kDramRegimeBytes = uint64_t{64} << 20;
-static int g_regime = 0;  // 0 auto, 1 force L2 regime, 2 force DRAM regime, 3 DRAM + deferral
+static int g_regime = 0;  // 0 auto, 1 force L2 regime (file-order layouts), 2 force DRAM regime
 void set_regime(int r) { g_regime = r; }
 
-template <int G, bool POW2, class OutT, int SRC, int KPT, int MINB, bool DEFER>
+template <int G, bool POW2, class OutT, int SRC, int KPT, int MINB, bool DEFER, bool HOTF>
 static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
                                 int minimal, cudaStream_t s, int sms, const RemapList& rl) {
-    auto kern = k_query_u64<G, POW2, OutT, KPT, SRC, MINB, (PH_DEFER && DEFER)>;
+    auto kern = k_query_u64<G, POW2, OutT, KPT, SRC, MINB, (PH_DEFER && DEFER), HOTF>;
     const int threads = g_threads_override > 0 ? g_threads_override : PH_THREADS;
     const int blocks = grid_for(kern, threads, (uint64_t)threads / 32 * 32 * KPT, n, sms);
     const uint32_t nlists = (uint32_t)blocks * (uint32_t)(threads / 32);
@@ -300,7 +319,7 @@ static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out
                               ? rl
                               : RemapList{nullptr, nullptr, nullptr, 0};
     cudaError_t e = launch_ex(ix, kern, blocks, threads, s, ix, src.ptr, static_cast<OutT*>(out),
-                              n, minimal, src.seq_words, src.kbits, use);
+                              n, minimal, src.seq_words, src.kbits, use, src.dyn_n);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e == cudaSuccess && use.idx) {
         k_remap_patch<OutT><<<(nlists + 7) / 8, 256, 0, s>>>(ix, use, nlists,
@@ -314,12 +333,23 @@ static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out
 template <int G, bool POW2, class OutT, int SRC>
 static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
                                 int minimal, cudaStream_t s, int sms, const RemapList& rl) {
-    const bool dram = g_regime >= 2 ||
-                      (g_regime == 0 && src.tuning == 0 && ix.P * ix.B > kDramRegimeBytes);
-    if (dram && g_regime == 3)  // experiment: DRAM tuning with the deferred remap
-        return launch_u64_k<G, POW2, OutT, SRC, 8, 1, true>(ix, src, out, n, minimal, s, sms, rl);
-    if (dram) return launch_u64_k<G, POW2, OutT, SRC, 8, 1, false>(ix, src, out, n, minimal, s, sms, rl);
-    return launch_u64_k<G, POW2, OutT, SRC, 4, 8, true>(ix, src, out, n, minimal, s, sms, rl);
+    const bool hotf = ix.hot_b < ix.B;
+    if constexpr (SRC == 2) {  // binned entries: pilots of the current group are L2-resident
+        if (hotf) return cudaErrorInvalidValue;  // the partitioned path needs the file order
+        return launch_u64_k<G, POW2, OutT, SRC, PH_L2_KPT, PH_L2_MINB, true, false>(ix, src, out, n, minimal, s,
+                                                                   sms, rl);
+    } else {
+        const bool dram = hotf || g_regime == 2 ||
+                          (g_regime == 0 && src.tuning == 0 && ix.P * ix.B > kDramRegimeBytes);
+        if (dram && hotf)
+            return launch_u64_k<G, POW2, OutT, SRC, 8, 1, false, true>(ix, src, out, n, minimal, s,
+                                                                       sms, rl);
+        if (dram)
+            return launch_u64_k<G, POW2, OutT, SRC, 8, 1, false, false>(ix, src, out, n, minimal,
+                                                                        s, sms, rl);
+        return launch_u64_k<G, POW2, OutT, SRC, PH_L2_KPT, PH_L2_MINB, true, false>(ix, src, out, n, minimal, s,
+                                                                   sms, rl);
+    }
 }
 
 template <class OutT, int SRC>
@@ -345,6 +375,10 @@ static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, con
                               void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                               int sms, const RemapList& rl) {
     if (n == 0) return cudaSuccess;
+    if (k.kind == 2)
+        return out_width == 4
+                   ? launch_u64_w<uint32_t, 2>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl)
+                   : launch_u64_w<uint64_t, 2>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl);
     if (k.kind == 1)
         return out_width == 4
                    ? launch_u64_w<uint32_t, 1>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl)
@@ -357,7 +391,7 @@ static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, con
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                              int sms, const RemapList& rl) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0}, out, out_width, n, minimal, s,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0, nullptr}, out, out_width, n, minimal, s,
                       sms, rl);
 }
 
@@ -366,7 +400,7 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                                cudaStream_t s, int sms, const RemapList& rl) {
     if (n_bases < (uint64_t)k) return cudaSuccess;
     const uint64_t n = n_bases - (uint64_t)k + 1;
-    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0},
+    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0, nullptr},
                       out, out_width, n, minimal, s, sms, rl);
 }
 
@@ -374,8 +408,16 @@ cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2
                                    const uint64_t* keys, void* out, int out_width, uint64_t n,
                                    int minimal, cudaStream_t s, int sms, const RemapList& rl,
                                    bool l2_tuning) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0}, out,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0, nullptr}, out,
                       out_width, n, minimal, s, sms, rl);
+}
+
+cudaError_t launch_query_bins(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* bins,
+                              const unsigned long long* dyn_n, uint64_t n_max, void* out,
+                              int out_width, int minimal, cudaStream_t s, int sms,
+                              const RemapList& rl) {
+    return launch_src(ix, gamma_kind, pow2, KeySrc{bins, 2, 0, 0, 1, dyn_n}, out, out_width, n_max,
+                      minimal, s, sms, rl);
 }
 
 // ---------------------------------------------------------------------------

@@ -23,7 +23,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libph_gpu.so")
+# PH_GPU_LIB: a tuning build of the same library (tools/; paper_2502_15539_b200/variants/)
+LIB_PATH = os.environ.get("PH_GPU_LIB") or os.path.join(_HERE, "libph_gpu.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -69,6 +70,9 @@ _L.ph_gpu_index_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
 _L.ph_gpu_verify_bijection.argtypes = [C.c_void_p, C.c_size_t, C.c_int, C.c_uint64, C.c_int,
                                        u64p, u64p]
 _L.ph_gpu_set_launch.argtypes = [C.c_int, C.c_int]
+_L.ph_gpu_set_partition.argtypes = [C.c_int]
+_L.ph_gpu_set_regime.argtypes = [C.c_int]
+_L.ph_gpu_index_set_l2_policy.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
 
 # status codes (ph_gpu.h)
 OK, E_INVALID, E_FORMAT, E_CUDA, E_KEYKIND, E_NOMEM, E_UNSUPPORTED = range(7)
@@ -99,6 +103,15 @@ def launch_count() -> int:
 
 def set_launch(threads_per_block: int = 0, blocks_per_sm: int = 0):
     _check(_L.ph_gpu_set_launch(threads_per_block, blocks_per_sm))
+
+
+def set_partition(mode: int):
+    """0 automatic, 1 never, 2 whenever the index allows (ph_gpu_set_partition)."""
+    _check(_L.ph_gpu_set_partition(mode))
+
+
+def set_regime(regime: int):
+    _check(_L.ph_gpu_set_regime(regime))
 
 
 def _is_torch(x):
@@ -143,6 +156,10 @@ class PtrHashIndex:
                                           out.element_size(), int(self.info.n if n is None else n),
                                           int(self.info.device), C.byref(oob), C.byref(dup)))
         return int(oob.value), int(dup.value)
+
+    def set_l2_policy(self, hot_bytes: int, flags: int = 0):
+        """Pilot layout / L2 policy (ph_gpu_index_set_l2_policy); results are unaffected."""
+        _check(_L.ph_gpu_index_set_l2_policy(self._h, hot_bytes, flags))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -327,3 +327,34 @@ def test_verify_bijection_on_device(ph, ref):
     nm = idx.query(dev(keys), minimal=False, out_width=8)
     P, S = idx.shape()[1:3]
     assert idx.verify_bijection(nm, n=P * S) == (0, 0)
+
+
+@pytest.mark.parametrize("hot_bytes,flags", [(0, 0), (0, 2), (4096, 0), (4096, 1), (4096, 2),
+                                             (1 << 16, 3)])
+def test_pilot_layouts_bitexact(ph, ref, hot_bytes, flags):
+    """ph_gpu_index_set_l2_policy: the hot-first layout (hot region of hot_bytes, with and
+    without the persisting window / evict_first cold loads) and the file order answer
+    identically to the reference, through the direct kernels and (file order) the
+    partitioned path, for u64 keys and k-mers."""
+    from oracle.bindings import corpus_u64_np
+    n = 300_000
+    keys = corpus_u64_np(0, n, 71)
+    ptrh = ref.build_u64(keys, ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    idx.set_l2_policy(hot_bytes, flags)
+    q = np.concatenate([keys, corpus_u64_np(0, n // 3, 72)])
+    for minimal in (True, False):
+        want = ri.query_u64(q, minimal, "loop", threads=THREADS)
+        for width in (4, 8):
+            assert np.array_equal(gpu_query(idx, q, minimal, width), want), (minimal, width)
+    if hot_bytes == 0:  # file order: the partitioned path applies
+        ph.set_partition(2)
+        try:
+            assert np.array_equal(gpu_query(idx, q, True, 4),
+                                  ri.query_u64(q, True, "loop", threads=THREADS))
+        finally:
+            ph.set_partition(0)
+    idx.set_l2_policy(64 << 20, 0)  # back to the default
+    assert np.array_equal(gpu_query(idx, keys, True, 8),
+                          ri.query_u64(keys, True, "loop", threads=THREADS))

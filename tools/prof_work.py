@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--minimal", type=int, default=1)
     ap.add_argument("--regimes", default="", help="comma list of ph_gpu_set_regime values to time")
     ap.add_argument("--partition", default="", help="comma list of ph_gpu_set_partition modes")
+    ap.add_argument("--layout", default="default", help="default | file (pilot layout)")
+    ap.add_argument("--no-persist", action="store_true",
+                    help="drop the persisting-L2 carve-out after the index is created")
     a = ap.parse_args()
     cfg = dict(bench.CONFIGS[a.config])
     if a.n:
@@ -39,6 +42,14 @@ def main():
     stream = torch.cuda.current_stream()
     W = bench.WORKLOADS[cfg["kind"]](a, cfg, _Dist(), lib, C.c_void_p(stream.cuda_stream))
     out = torch.empty(W.nq, dtype=torch.int32, device="cuda")
+    if a.no_persist:
+        lib.phb_set_persist.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_float, C.c_size_t]
+        assert lib.phb_set_persist(C.c_void_p(stream.cuda_stream), None, 0, 0.0, 0) == 0
+    from paper_2502_15539_b200 import ph_gpu
+    if a.layout == "file":  # file-order pilots, no persisting window (partition-capable)
+        W.idx.set_l2_policy(0, 2)
+    if a.ncu and a.partition:  # profile the first listed partition mode
+        ph_gpu.set_partition(int(a.partition.split(",")[0]))
     W.query(out, bool(a.minimal), stream.cuda_stream)
     torch.cuda.synchronize()
     if a.ncu:

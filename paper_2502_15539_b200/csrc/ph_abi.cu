@@ -322,9 +322,14 @@ struct DeferScratch {
 // on the default hot-first layout (profiles/r01_partition_*.txt).
 std::atomic<int> g_partition{0};  // 0 auto, 1 off, 2 force when the layout allows
 
-uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n) {
+uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n, int out_width) {
     const int mode = g_partition.load();
     if (mode == 1 || !ix->pool || ix->dev.hot_b < ix->dev.B) return 0;  // needs file order
+    // pass B stores non-minimal slots in the output width
+    if (out_width == PH_OUT_U32 && ix->info.parts * ix->info.slots_per_part > (uint64_t{1} << 32))
+        return 0;
+    // pass C lists remap indices as u32
+    if (ix->info.parts * ix->info.slots_per_part - ix->info.n >= (uint64_t{1} << 32)) return 0;
     const uint64_t pb = ix->info.pilot_bytes;
     if (mode == 0 && (pb <= (uint64_t{64} << 20) || n < pb / 2 || ix->dev.window_bytes))
         return 0;
@@ -348,13 +353,10 @@ cudaError_t run_partitioned(const ph_gpu_index* ix, const uint64_t* keys, int sr
         cudaGetLastError();
         return cudaErrorMemoryAllocation;
     }
-    cudaError_t e;
-    {
-        DeferScratch ds(ix, n, minimal, s);
-        e = phg::launch_query_partitioned(ix->dev, ix->info.bucket_fn, ix->info.pow2, keys,
-                                          src_kind, seq_words, kbits, out, out_width, n, minimal,
-                                          G, scratch, s, ix->sms, ds.rl);
-    }
+    const cudaError_t e = phg::launch_query_partitioned(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                                        keys, src_kind, seq_words, kbits, out,
+                                                        out_width, n, minimal, G, scratch, s,
+                                                        ix->sms);
     cudaFreeAsync(scratch, s);
     return e;
 }
@@ -571,7 +573,7 @@ int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, v
     if (n == 0) return PH_OK;
     if (!d_keys || !d_out) return fail(PH_E_INVALID, "null key or output pointer");
     DeviceGuard g(ix->device);
-    if (const uint32_t G = partition_groups(ix, n)) {
+    if (const uint32_t G = partition_groups(ix, n, out_width)) {
         const cudaError_t pe = run_partitioned(ix, d_keys, 0, 0, 0, d_out, out_width, n, minimal,
                                                G, static_cast<cudaStream_t>(stream));
         if (pe != cudaErrorMemoryAllocation)
@@ -809,7 +811,7 @@ int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n
     if (!d_seq || !d_out) return fail(PH_E_INVALID, "null sequence or output pointer");
     DeviceGuard g(ix->device);
     const uint64_t nwin = n_bases - (uint64_t)k + 1;
-    if (const uint32_t G = partition_groups(ix, nwin)) {
+    if (const uint32_t G = partition_groups(ix, nwin, out_width)) {
         const cudaError_t pe = run_partitioned(ix, d_seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k),
                                                d_out, out_width, nwin, minimal, G,
                                                static_cast<cudaStream_t>(stream));

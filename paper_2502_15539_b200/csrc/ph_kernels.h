@@ -12,26 +12,39 @@ namespace phg {
 
 // Launch `kernel` with the index's persisting-L2 access-policy window over the hot
 // pilot region (a per-launch attribute: the caller's stream is not modified).
+// pdl: programmatic dependent launch (cudaLaunchAttributeProgrammaticStreamSerialization).
 template <class... KArgs, class... Args>
-inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
-                             unsigned block, cudaStream_t s, Args... args) {
+inline cudaError_t launch_ex_pdl(const DevIndex& ix, bool pdl, void (*kernel)(KArgs...),
+                                 unsigned grid, unsigned block, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    unsigned na = 0;
     if (ix.window_bytes) {
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<uint8_t*>(ix.pilots);
-        attr[0].val.accessPolicyWindow.num_bytes = ix.window_bytes;
-        attr[0].val.accessPolicyWindow.hitRatio = ix.window_hit_ratio;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = const_cast<uint8_t*>(ix.pilots);
+        attr[na].val.accessPolicyWindow.num_bytes = ix.window_bytes;
+        attr[na].val.accessPolicyWindow.hitRatio = ix.window_hit_ratio;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        na++;
     }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        na++;
+    }
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+template <class... KArgs, class... Args>
+inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
+                             unsigned block, cudaStream_t s, Args... args) {
+    return launch_ex_pdl(ix, false, kernel, grid, block, s, args...);
 }
 
 // Scratch for the deferred remap (k_remap_patch); idx == nullptr selects the inline
@@ -67,10 +80,11 @@ cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2
 
 // Pass B of the partitioned path: bins[0, min(*dyn_n, n_max)) (device-side count), answered
 // into out[] at the same entry index with the L2-resident tuning.
+// Non-minimal slots only; pdl: launch as a programmatic dependent of the preceding kernel
+// (the kernels of consecutive groups do not depend on one another).
 cudaError_t launch_query_bins(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* bins,
                               const unsigned long long* dyn_n, uint64_t n_max, void* out,
-                              int out_width, int minimal, cudaStream_t s, int sms,
-                              const RemapList& rl);
+                              int out_width, cudaStream_t s, int sms, bool pdl);
 
 // Partitioned path (ph_partition.cu). src_kind 0: keys = u64 keys; 1: keys = packed
 // sequence (seq_words, kbits), n = number of windows. scratch >= partition_scratch_bytes.
@@ -79,7 +93,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
                                      const uint64_t* keys, int src_kind, uint64_t seq_words,
                                      uint32_t kbits, void* out, int out_width, uint64_t n,
                                      int minimal, uint32_t G, void* scratch, cudaStream_t s,
-                                     int sms, const RemapList& rl);
+                                     int sms);
 
 cudaError_t launch_relayout(const uint8_t* src, uint8_t* dst, uint64_t P, uint64_t B, uint64_t H,
                             cudaStream_t s);

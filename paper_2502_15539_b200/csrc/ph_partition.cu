@@ -26,8 +26,10 @@
 // streamed, against the direct kernel's 12 B streamed + one DRAM row activation per query.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ph_device.cuh"
 #include "ph_kernels.h"
@@ -38,8 +40,8 @@ constexpr int kBinThreads = 256;
 constexpr int kBinPerThread = 16;
 constexpr uint32_t kTileKeys = kBinThreads * kBinPerThread;  // 4096 keys per tile
 constexpr int kBinCtas = 4;    // CTAs per SM (registers: 64 per thread)
-constexpr int kUnbinCtas = 5;
 constexpr int kMaxGroups = 64;
+constexpr uint16_t kPadPos = 0xffff;  // position of a run's padding entry (never a tile position)
 // ctrl[]: per-group cursors [0, kMaxGroups), spill cursor
 constexpr int kCtrlSpill = kMaxGroups;
 constexpr int kCtrlWords = kMaxGroups + 1;
@@ -65,6 +67,19 @@ __device__ __forceinline__ uint64_t part_kmer(const uint64_t* __restrict__ seq, 
     return kbits == 64 ? top : top >> (64 - kbits);
 }
 
+// Reserves a run for c entries of group g: c rounded up to a multiple of 8 entries, so
+// every run starts 64-B aligned in bins[] and 16-B aligned in bpos[] / slots[] (the bulk
+// copies of passes A and C need that). Group regions hold `cap` entries; a run that does
+// not fit goes to the spill region after them.
+__device__ __forceinline__ uint64_t reserve_run(unsigned long long* ctrl, uint32_t g, uint32_t c,
+                                                uint32_t G, uint64_t cap) {
+    if (!c) return 0;
+    const unsigned long long c8 = (c + 7u) & ~7u;
+
+    const uint64_t off = atomicAdd(ctrl + g, c8);
+    return off + c8 <= cap ? g * cap + off : G * cap + atomicAdd(ctrl + kCtrlSpill, c8);
+}
+
 __device__ __forceinline__ void st_cs_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -83,7 +98,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtas) k_bin(
     uint64_t seed, uint32_t G, uint64_t cap, unsigned long long* __restrict__ ctrl,
     uint64_t* __restrict__ runoff, uint16_t* __restrict__ runcnt, uint64_t* __restrict__ bins,
     uint16_t* __restrict__ bpos) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem);
     uint32_t* spg = reinterpret_cast<uint32_t*>(sk + kTileKeys);  // tile position | group << 16
     __shared__ uint32_t cnt[2][kMaxGroups];
@@ -143,13 +158,8 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtas) k_bin(
             for (int h = 0; h < 2; h++) {
                 const uint32_t g = 2 * lane + h, c = h ? c1 : c0;
                 if (g < G) {
-                    uint64_t off = 0;
-                    if (c) {
-                        off = atomicAdd(ctrl + g, (unsigned long long)c);
-                        off = off + c <= cap
-                                  ? g * cap + off
-                                  : G * cap + atomicAdd(ctrl + kCtrlSpill, (unsigned long long)c);
-                    }
+                    const uint64_t off = reserve_run(ctrl, g, c, G, cap);
+                    for (uint32_t i = c; i < ((c + 7u) & ~7u); i++) bpos[off + i] = kPadPos;
                     delta[g] = off - lbase[g];
                     runoff[t * G + g] = off;
                     runcnt[t * G + g] = (uint16_t)c;
@@ -182,74 +192,323 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtas) k_bin(
     }
 }
 
-// Pass C. Per tile: the G runs are laid end to end (run g at lbase[g]); rid[e] names the
-// run of staged entry e. Every thread issues its 16 (position, slot) loads before storing
-// any into the shared-memory tile, which is then written out in order.
-template <class OutT>
-__global__ void __launch_bounds__(kBinThreads, sizeof(OutT) == 4 ? kUnbinCtas : kUnbinCtas - 1) k_unbin(
-    uint64_t n, uint32_t G, const uint64_t* __restrict__ runoff,
-    const uint16_t* __restrict__ runcnt, const uint16_t* __restrict__ bpos,
-    const OutT* __restrict__ slots, OutT* __restrict__ out) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    OutT* stage = reinterpret_cast<OutT*>(smem);
-    uint8_t* rid = reinterpret_cast<uint8_t*>(stage + kTileKeys);
-    __shared__ uint32_t rc[kMaxGroups];
-    __shared__ uint32_t lbase[kMaxGroups];
-    __shared__ uint64_t delta[kMaxGroups];  // run offset - staged offset
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA engine, cp.async.bulk) variants of passes A and C: tiles of keys arrive in
+// shared memory by bulk loads completing on an mbarrier (double-buffered, issued two tiles
+// ahead), and every staged run leaves with one bulk store per array. Threads only rank,
+// place and scatter in shared memory. Used when the key array is 16-B aligned.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared, completes `bytes` on bar (16-B aligned, multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+// shared -> global, bulk-group completion (16-B aligned, multiple of 16)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                     dst),
+                 "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+constexpr uint32_t kStageEntries = kTileKeys + 7 * kMaxGroups;  // runs padded to 8 entries
+constexpr int kTmaGroups = 32;
+constexpr uint32_t kRemapCap = 128;  // pass C: remap list entries per tile (k_remap_tiles)  // pass A's bulk-copy variant: G <= 32 (lane = group)
+constexpr uint32_t kBinTmaStage = kTileKeys + 8 * kTmaGroups;  // (a multiple of 8)
+#ifndef PH_BIN_TMA_THREADS
+#define PH_BIN_TMA_THREADS 512
+#endif
+constexpr int kBinTmaThreads = PH_BIN_TMA_THREADS;
+constexpr size_t kBinTmaSmem = 2 * kTileKeys * 8 + kBinTmaStage * (8 + 2);
+
+// Pass A, bulk-copy variant (u64 keys, 16-B aligned key array).
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
+    const uint64_t* __restrict__ keys, uint64_t n, uint64_t seed, uint32_t G, uint64_t cap,
+    unsigned long long* __restrict__ ctrl, uint64_t* __restrict__ runoff,
+    uint16_t* __restrict__ runcnt, uint64_t* __restrict__ bins, uint16_t* __restrict__ bpos) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* in = reinterpret_cast<uint64_t*>(smem);  // [2][kTileKeys]
+    uint64_t* sk = in + 2 * kTileKeys;                   // staged keys, runs 8-aligned
+    uint16_t* sp = reinterpret_cast<uint16_t*>(sk + kBinTmaStage);
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ uint32_t cnt[2][kTmaGroups];
+    __shared__ uint32_t lb8[kTmaGroups];
+    __shared__ uint32_t rc[kTmaGroups];
+    __shared__ uint64_t roff[kTmaGroups];
+    constexpr int PER = kTileKeys / THREADS;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t nfull = n / kTileKeys;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    if (tid < kTmaGroups) cnt[0][tid] = 0;
+    __syncthreads();
+    auto issue = [&](uint64_t t, int b) {  // thread 0: bulk-load full tile t into buffer b
+        mbar_expect_tx(&bar[b], kTileKeys * 8);
+        bulk_g2s(in + b * kTileKeys, keys + t * kTileKeys, kTileKeys * 8, &bar[b], pol);
+    };
+    if (tid == 0) {
+        if (blockIdx.x < nfull) issue(blockIdx.x, 0);
+        if (blockIdx.x + gridDim.x < nfull) issue(blockIdx.x + gridDim.x, 1);
+    }
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
+        const int b = it & 1;
         const uint64_t t0 = t * kTileKeys;
         const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
+        uint64_t k[PER];
+        if (t < nfull) {
+            mbar_wait(&bar[b], (it >> 1) & 1);
+#pragma unroll
+            for (int j = 0; j < PER; j++) k[j] = in[b * kTileKeys + j * THREADS + tid];
+        } else {
+#pragma unroll
+            for (int j = 0; j < PER; j++) {
+                const uint32_t e = (uint32_t)j * THREADS + tid;
+                k[j] = e < valid ? __ldcs(keys + t0 + e) : 0;
+            }
+        }
+        uint32_t* c_ = cnt[b];
+        uint32_t gr[PER];  // group << 16 | rank
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            if ((uint32_t)j * THREADS + tid < valid) {
+                const uint32_t g = group_of(k[j], seed, G);
+                gr[j] = g << 16 | atomicAdd(&c_[g], 1u);
+            }
+        }
+        __syncthreads();  // #1: buffer b consumed, counts final
+        if (tid == 0 && t + 2 * (uint64_t)gridDim.x < nfull) issue(t + 2 * (uint64_t)gridDim.x, b);
+        if (tid < kTmaGroups) cnt[b ^ 1][tid] = 0;  // next tile's counters
+        // warp 0 (lane = group): the run reservation is issued first (its latency overlaps
+        // the scan, barrier #2 and the staging)
+        uint32_t c = 0;
+        unsigned long long a = 0;
         if (warp == 0) {
-            const uint32_t g0 = 2 * lane;
-            const uint32_t c0 = g0 < G ? __ldg(runcnt + t * G + g0) : 0;
-            const uint32_t c1 = g0 + 1 < G ? __ldg(runcnt + t * G + g0 + 1) : 0;
-            const uint64_t o0 = g0 < G ? __ldg(runoff + t * G + g0) : 0;
-            const uint64_t o1 = g0 + 1 < G ? __ldg(runoff + t * G + g0 + 1) : 0;
-            uint32_t x = c0 + c1;
+            c = lane < G ? c_[lane] : 0;
+            if (c) a = atomicAdd(ctrl + lane, (unsigned long long)((c + 7) & ~7u));
+            bulk_wait_read();  // the previous tile's run stores have read the staging buffer
+            const uint32_t p8 = (c + 7) & ~7u;
+            uint32_t x = p8;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, x, o);
                 if (lane >= (unsigned)o) x += y;
             }
-            x -= c0 + c1;
-            lbase[g0] = x;
-            lbase[g0 + 1] = x + c0;
-            delta[g0] = o0 - x;
-            delta[g0 + 1] = o1 - (x + c0);
-            rc[g0] = c0;
-            rc[g0 + 1] = c1;
+            lb8[lane] = x - p8;
+            rc[lane] = c;
         }
-        __syncthreads();
-        for (uint32_t g = warp; g < G; g += kBinThreads / 32) {
-            const uint32_t c = rc[g], lb = lbase[g];
-            for (uint32_t i = lane; i < c; i += 32) rid[lb + i] = (uint8_t)g;
-        }
-        __syncthreads();
-        uint16_t pv[kBinPerThread];
-        OutT sv[kBinPerThread];
+        __syncthreads();  // #2: staging free, lb8 final
 #pragma unroll
-        for (int j = 0; j < kBinPerThread; j++) {
-            const uint32_t e = (uint32_t)j * kBinThreads + tid;
-            if (e < valid) {
-                const uint64_t src = delta[rid[e]] + e;
-                pv[j] = __ldcs(bpos + src);
-                sv[j] = __ldcs(slots + src);
+        for (int j = 0; j < PER; j++) {
+            const uint32_t pos = (uint32_t)j * THREADS + tid;
+            if (pos < valid) {
+                const uint32_t e = lb8[gr[j] >> 16] + (gr[j] & 0xffffu);
+                sk[e] = k[j];
+                sp[e] = (uint16_t)pos;
             }
         }
+        if (warp == 0 && lane < G) {  // consume the reservation (spill if the region is full)
+            const unsigned long long c8 = (c + 7u) & ~7u;
+            for (uint32_t i = c; i < c8; i++) sp[lb8[lane] + i] = kPadPos;  // padding entries
+            const uint64_t off = !c ? 0
+                                 : a + c8 <= cap ? lane * cap + a
+                                                 : G * cap + atomicAdd(ctrl + kCtrlSpill, c8);
+            roff[lane] = off;
+            runoff[t * G + lane] = off;
+            runcnt[t * G + lane] = (uint16_t)c;
+        }
+        fence_async_smem();
+        __syncthreads();  // #3: staged; run offsets known
+        if (warp == 0) {  // lane issues the bulk stores of its group's run
+            if (lane < G && rc[lane]) {
+                const uint32_t c8 = (rc[lane] + 7) & ~7u, l = lb8[lane];
+                bulk_s2g(bins + roff[lane], sk + l, c8 * 8, pol);
+                bulk_s2g(bpos + roff[lane], sp + l, c8 * 2, pol);
+            }
+            bulk_commit();
+        }
+    }
+    if (warp == 0) bulk_wait_all();
+}
+
+// Pass C, bulk-copy variant: the tile's runs (8-entry aligned) arrive by bulk loads two
+// tiles ahead (double-buffered), are scattered by position into the output tile in shared
+// memory, and the output tile leaves with one bulk store when `out` is 16-B aligned.
+template <class OutT>
+struct UnbinTma {
+    static constexpr size_t kIn = (size_t)kStageEntries * (sizeof(OutT) + 2);  // one buffer
+    static constexpr size_t kSmem = 2 * kIn + (size_t)kTileKeys * sizeof(OutT);
+};
+
+template <class OutT>
+__global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
+    const DevIndex ix, int minimal, uint64_t n, uint32_t G, const uint64_t* __restrict__ runoff,
+    const uint16_t* __restrict__ runcnt, const uint16_t* __restrict__ bpos,
+    const OutT* __restrict__ slots, OutT* __restrict__ out, uint16_t* __restrict__ rl_pos,
+    uint32_t* __restrict__ rl_idx, uint32_t* __restrict__ rl_cnt) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    OutT* stage = reinterpret_cast<OutT*>(smem + 2 * UnbinTma<OutT>::kIn);
+    __shared__ __align__(8) uint64_t bar[2];
+    // remap_slot (index.hpp:98-100) of the tile's slots >= n: listed per tile for
+    // k_remap_tiles (the decode's dependent reads stay off this kernel's critical path)
+    __shared__ uint32_t nrem;
+    __shared__ uint32_t mtot[2];             // per buffer: staged entries (runs padded to 8)
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    const uint64_t pol = policy_evict_first();
+    auto bufs = [&](int b, OutT*& sv, uint16_t*& pv) {
+        sv = reinterpret_cast<OutT*>(smem + b * UnbinTma<OutT>::kIn);
+        pv = reinterpret_cast<uint16_t*>(sv + kStageEntries);
+    };
+    // warp 0: bulk-load tile t's runs into buffer b
+    auto issue = [&](uint64_t t, int b) {
+        const uint32_t g0 = 2 * lane;
+        const uint32_t c0 = g0 < G ? __ldg(runcnt + t * G + g0) : 0;
+        const uint32_t c1 = g0 + 1 < G ? __ldg(runcnt + t * G + g0 + 1) : 0;
+        const uint64_t o0 = g0 < G ? __ldg(runoff + t * G + g0) : 0;
+        const uint64_t o1 = g0 + 1 < G ? __ldg(runoff + t * G + g0 + 1) : 0;
+        const uint32_t p0 = (c0 + 7) & ~7u, p1 = (c1 + 7) & ~7u;
+        uint32_t x = p0 + p1;
 #pragma unroll
-        for (int j = 0; j < kBinPerThread; j++)
-            if ((uint32_t)j * kBinThreads + tid < valid) stage[pv[j]] = sv[j];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= (unsigned)o) x += y;
+        }
+        const uint32_t total = __shfl_sync(kFull, x, 31);
+        x -= p0 + p1;
+        if (lane == 0) {
+            mtot[b] = total;
+            mbar_expect_tx(&bar[b], total * (uint32_t)(sizeof(OutT) + 2));
+        }
+        __syncwarp();
+        OutT* sv;
+        uint16_t* pv;
+        bufs(b, sv, pv);
+        if (p0) {
+            bulk_g2s(sv + x, slots + o0, p0 * (uint32_t)sizeof(OutT), &bar[b], pol);
+            bulk_g2s(pv + x, bpos + o0, p0 * 2, &bar[b], pol);
+        }
+        if (p1) {
+            bulk_g2s(sv + x + p0, slots + o1, p1 * (uint32_t)sizeof(OutT), &bar[b], pol);
+            bulk_g2s(pv + x + p0, bpos + o1, p1 * 2, &bar[b], pol);
+        }
+    };
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+        if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+    }
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
+        const int b = it & 1;
+        const uint64_t t0 = t * kTileKeys;
+        const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
+        mbar_wait(&bar[b], (it >> 1) & 1);
+        if (tid == 0) {
+            bulk_wait_read();  // the previous output tile has left `stage`
+            nrem = 0;
+        }
         __syncthreads();
-        {
+        OutT* sv;
+        uint16_t* pv;
+        bufs(b, sv, pv);
+        // every staged entry in parallel; padding entries carry position kPadPos
+        const uint32_t total = mtot[b];
 #pragma unroll 4
-            for (int j = 0; j < kBinPerThread; j++) {
-                const uint32_t e = (uint32_t)j * kBinThreads + tid;
-                if (e < valid) st_stream(out + t0 + e, stage[e]);
+        for (uint32_t e = tid; e < total; e += kBinThreads) {
+            const uint16_t p = pv[e];
+            const uint64_t v = sv[e];
+            if (p == kPadPos) continue;
+            if (minimal && v >= ix.n) {
+                const uint32_t r = atomicAdd(&nrem, 1u);
+                if (r < kRemapCap) {
+                    rl_pos[t * kRemapCap + r] = p;
+                    rl_idx[t * kRemapCap + r] = (uint32_t)(v - ix.n);
+                    stage[p] = 0;  // patched by k_remap_tiles
+                } else {
+                    stage[p] = (OutT)remap_get_cold(ix, v - ix.n);  // list full
+                }
+            } else {
+                stage[p] = (OutT)v;
             }
         }
+        fence_async_smem();
         __syncthreads();
+        if (minimal && tid == 0) rl_cnt[t] = min(nrem, kRemapCap);
+        if (vec && valid == kTileKeys) {
+            if (tid == 0) {
+                bulk_s2g(out + t0, stage, kTileKeys * (uint32_t)sizeof(OutT), pol);
+                bulk_commit();
+            }
+        } else {
+            for (uint32_t e = tid; e < valid; e += kBinThreads) st_stream(out + t0 + e, stage[e]);
+        }
+        if (warp == 0 && t + 2 * (uint64_t)gridDim.x < ntiles) issue(t + 2 * (uint64_t)gridDim.x, b);
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+// Pass C's remap lists: one warp per tile decodes its slots >= n and patches the outputs.
+template <class OutT>
+__global__ void __launch_bounds__(256) k_remap_tiles(const DevIndex ix, uint64_t ntiles,
+                                                     const uint16_t* __restrict__ rl_pos,
+                                                     const uint32_t* __restrict__ rl_idx,
+                                                     const uint32_t* __restrict__ rl_cnt,
+                                                     OutT* __restrict__ out) {
+    const unsigned lane = threadIdx.x & 31;
+    for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+         t += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t c = rl_cnt[t];
+        for (uint32_t i = lane; i < c; i += 32)
+            out[t * kTileKeys + rl_pos[t * kRemapCap + i]] =
+                (OutT)remap_get(ix, rl_idx[t * kRemapCap + i]);
     }
 }
 
@@ -257,16 +516,18 @@ __global__ void __launch_bounds__(kBinThreads, sizeof(OutT) == 4 ? kUnbinCtas : 
 namespace {
 struct Layout {
     uint64_t cap, ntiles, nent;
-    uint64_t o_runoff, o_runcnt, o_bins, o_bpos, o_slots, total;
+    uint64_t o_runoff, o_runcnt, o_bins, o_bpos, o_slots, o_rlpos, o_rlidx, o_rlcnt, total;
 };
 Layout layout(uint64_t n, uint32_t G, int out_width) {
     auto al = [](uint64_t b) { return (b + 255) & ~uint64_t{255}; };
     Layout L;
     const uint64_t per = (n + G - 1) / G;
-    L.cap = per + 16 * (uint64_t)std::ceil(std::sqrt((double)per)) + kTileKeys;
-    L.cap = (L.cap + 255) & ~uint64_t{255};
     L.ntiles = (n + kTileKeys - 1) / kTileKeys;
-    L.nent = G * L.cap + n;
+    // n/G + 16 sigma + one tile + up to 7 padding entries per tile (8-entry aligned runs)
+    L.cap = per + 16 * (uint64_t)std::ceil(std::sqrt((double)per)) + kTileKeys + 7 * L.ntiles;
+    L.cap = (L.cap + 255) & ~uint64_t{255};
+    // spill: worst case every entry, each run padded by up to 7
+    L.nent = G * L.cap + n + 7 * std::min<uint64_t>(n, L.ntiles * G);
     uint64_t o = al(kCtrlWords * 8);
     L.o_runoff = o;
     o += al(L.ntiles * G * 8);
@@ -278,6 +539,12 @@ Layout layout(uint64_t n, uint32_t G, int out_width) {
     o += al(L.nent * 2);
     L.o_slots = o;
     o += al(L.nent * (uint64_t)out_width);
+    L.o_rlpos = o;
+    o += al(L.ntiles * kRemapCap * 2);
+    L.o_rlidx = o;
+    o += al(L.ntiles * kRemapCap * 4);
+    L.o_rlcnt = o;
+    o += al(L.ntiles * 4);
     L.total = o;
     return L;
 }
@@ -291,7 +558,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
                                      const uint64_t* keys, int src_kind, uint64_t seq_words,
                                      uint32_t kbits, void* out, int out_width, uint64_t n,
                                      int minimal, uint32_t G, void* scratch, cudaStream_t s,
-                                     int sms, const RemapList& rl) {
+                                     int sms) {
     if (n == 0) return cudaSuccess;
     if (G < 1 || G > (uint32_t)kMaxGroups) return cudaErrorInvalidValue;
     const Layout L = layout(n, G, out_width);
@@ -302,6 +569,9 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
     auto* bins = reinterpret_cast<uint64_t*>(base + L.o_bins);
     auto* bpos = reinterpret_cast<uint16_t*>(base + L.o_bpos);
     void* slots = base + L.o_slots;
+    auto* rl_pos = reinterpret_cast<uint16_t*>(base + L.o_rlpos);
+    auto* rl_idx = reinterpret_cast<uint32_t*>(base + L.o_rlidx);
+    auto* rl_cnt = reinterpret_cast<uint32_t*>(base + L.o_rlcnt);
 
     cudaError_t e = cudaMemsetAsync(ctrl, 0, kCtrlWords * 8, s);
     if (e != cudaSuccess) return e;
@@ -309,18 +579,24 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
     // (per device and cheap: set on every call)
     cudaFuncSetAttribute(k_bin<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
     cudaFuncSetAttribute(k_bin<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
-    cudaFuncSetAttribute(k_unbin<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kTileKeys * 9));
     const uint64_t want = L.ntiles;
     const int grid_a = (int)(want < (uint64_t)sms * kBinCtas ? want : (uint64_t)sms * kBinCtas);
-    const uint64_t ctas_c = (uint64_t)sms * (out_width == 4 ? kUnbinCtas : kUnbinCtas - 1);
-    const int grid_c = (int)(want < ctas_c ? want : ctas_c);
-    if (src_kind == 1)
+    const bool tma = src_kind == 0 && G <= (uint32_t)kTmaGroups &&
+                     (reinterpret_cast<uintptr_t>(keys) & 15) == 0 &&
+                     !std::getenv("PH_GPU_NO_TMA");
+    if (tma) {
+        cudaFuncSetAttribute(k_bin_tma<kBinTmaThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kBinTmaSmem);
+        const int grid_t = (int)(want < (uint64_t)sms * 2 ? want : (uint64_t)sms * 2);
+        k_bin_tma<kBinTmaThreads><<<grid_t, kBinTmaThreads, kBinTmaSmem, s>>>(
+            keys, n, ix.seed, G, L.cap, ctrl, runoff, runcnt, bins, bpos);
+    } else if (src_kind == 1) {
         k_bin<1><<<grid_a, kBinThreads, smem_a, s>>>(keys, n, seq_words, kbits, ix.seed, G, L.cap,
                                                    ctrl, runoff, runcnt, bins, bpos);
-    else
+    } else {
         k_bin<0><<<grid_a, kBinThreads, smem_a, s>>>(keys, n, 0, 0, ix.seed, G, L.cap, ctrl, runoff,
                                                    runcnt, bins, bpos);
+    }
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // B: the query kernel over the entries, one L2-sized pilot slice after another
@@ -329,22 +605,45 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
     ixb.window_bytes = 0;
     ixb.pilot_evict_normal = 1;
     ixb.cold_evict_first = 0;
+    // Pass B answers non-minimal slots (remap_slot happens in pass C), so its launches are
+    // independent of one another: each after the first is a programmatic dependent launch
+    // whose CTAs fill the SMs as the previous group's drain.
     uint8_t* sl = static_cast<uint8_t*>(slots);
     for (uint32_t g = 0; g <= G; g++) {  // g == G: the spill region
         const uint64_t off = g * L.cap;
-        e = launch_query_bins(ixb, gamma_kind, pow2, bins + off, ctrl + (g < G ? g : kCtrlSpill), g < G ? L.cap : n,
-                              sl + off * out_width, out_width, minimal, s, sms, rl);
+        e = launch_query_bins(ixb, gamma_kind, pow2, bins + off, ctrl + (g < G ? g : kCtrlSpill),
+                              g < G ? L.cap : n, sl + off * out_width, out_width, s, sms,
+                              /*pdl=*/g > 0);
         if (e != cudaSuccess) return e;
     }
-    const size_t smem_c = kTileKeys * (size_t)(out_width + 1);
-    if (out_width == 4)
-        k_unbin<uint32_t><<<grid_c, kBinThreads, smem_c, s>>>(n, G, runoff, runcnt, bpos,
-                                                            static_cast<const uint32_t*>(slots),
-                                                            static_cast<uint32_t*>(out));
-    else
-        k_unbin<uint64_t><<<grid_c, kBinThreads, smem_c, s>>>(n, G, runoff, runcnt, bpos,
-                                                            static_cast<const uint64_t*>(slots),
-                                                            static_cast<uint64_t*>(out));
+    {
+        const size_t sm4 = UnbinTma<uint32_t>::kSmem, sm8 = UnbinTma<uint64_t>::kSmem;
+        cudaFuncSetAttribute(k_unbin_tma<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm4);
+        cudaFuncSetAttribute(k_unbin_tma<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm8);
+        const uint64_t ctas = (uint64_t)sms * (out_width == 4 ? 3 : 1);
+        const int grid_t = (int)(want < ctas ? want : ctas);
+        if (out_width == 4)
+            k_unbin_tma<uint32_t><<<grid_t, kBinThreads, sm4, s>>>(
+                ix, minimal, n, G, runoff, runcnt, bpos, static_cast<const uint32_t*>(slots),
+                static_cast<uint32_t*>(out), rl_pos, rl_idx, rl_cnt);
+        else
+            k_unbin_tma<uint64_t><<<grid_t, kBinThreads, sm8, s>>>(
+                ix, minimal, n, G, runoff, runcnt, bpos, static_cast<const uint64_t*>(slots),
+                static_cast<uint64_t*>(out), rl_pos, rl_idx, rl_cnt);
+        note_launch();
+        if (minimal) {
+            const uint64_t wb = (L.ntiles + 7) / 8;  // 8 warps (tiles) per block
+            const int gr = (int)(wb < (uint64_t)sms * 8 ? wb : (uint64_t)sms * 8);
+            if (out_width == 4)
+                k_remap_tiles<uint32_t><<<gr, 256, 0, s>>>(ix, L.ntiles, rl_pos, rl_idx, rl_cnt,
+                                                           static_cast<uint32_t*>(out));
+            else
+                k_remap_tiles<uint64_t><<<gr, 256, 0, s>>>(ix, L.ntiles, rl_pos, rl_idx, rl_cnt,
+                                                           static_cast<uint64_t*>(out));
+        }
+    }
     note_launch();
     return cudaGetLastError();
 }

@@ -168,6 +168,8 @@ __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex i
     // SRC = 2 (the partitioned path's pass B): u64 entries whose count (<= nkeys_arg) is
     // only known on the device (written by pass A): no host synchronisation between passes.
     const uint64_t nkeys = SRC == 2 ? min((uint64_t)*dyn_n, nkeys_arg) : nkeys_arg;
+    // a dependent launch of the next group may start filling SMs as this one's CTAs drain
+    if (SRC == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -293,6 +295,7 @@ struct KeySrc {
     uint32_t kbits;
     int tuning;  // 0 = by pilot size, 1 = L2-resident tuning (the partitioned path's pass B)
     const unsigned long long* dyn_n;
+    bool pdl;  // programmatic dependent launch (partitioned pass B)
 };
 
 // Two tunings of the same kernel, chosen per index by the pilot array's size
@@ -318,8 +321,9 @@ static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out
                            rl.cap / nlists >= 32)
                               ? rl
                               : RemapList{nullptr, nullptr, nullptr, 0};
-    cudaError_t e = launch_ex(ix, kern, blocks, threads, s, ix, src.ptr, static_cast<OutT*>(out),
-                              n, minimal, src.seq_words, src.kbits, use, src.dyn_n);
+    cudaError_t e = launch_ex_pdl(ix, src.pdl, kern, blocks, threads, s, ix, src.ptr,
+                                  static_cast<OutT*>(out), n, minimal, src.seq_words, src.kbits,
+                                  use, src.dyn_n);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e == cudaSuccess && use.idx) {
         k_remap_patch<OutT><<<(nlists + 7) / 8, 256, 0, s>>>(ix, use, nlists,
@@ -391,7 +395,7 @@ static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, con
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                              int sms, const RemapList& rl) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0, nullptr}, out, out_width, n, minimal, s,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0, nullptr, false}, out, out_width, n, minimal, s,
                       sms, rl);
 }
 
@@ -400,7 +404,7 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                                cudaStream_t s, int sms, const RemapList& rl) {
     if (n_bases < (uint64_t)k) return cudaSuccess;
     const uint64_t n = n_bases - (uint64_t)k + 1;
-    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0, nullptr},
+    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0, nullptr, false},
                       out, out_width, n, minimal, s, sms, rl);
 }
 
@@ -408,16 +412,15 @@ cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2
                                    const uint64_t* keys, void* out, int out_width, uint64_t n,
                                    int minimal, cudaStream_t s, int sms, const RemapList& rl,
                                    bool l2_tuning) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0, nullptr}, out,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0, nullptr, false}, out,
                       out_width, n, minimal, s, sms, rl);
 }
 
 cudaError_t launch_query_bins(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* bins,
                               const unsigned long long* dyn_n, uint64_t n_max, void* out,
-                              int out_width, int minimal, cudaStream_t s, int sms,
-                              const RemapList& rl) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{bins, 2, 0, 0, 1, dyn_n}, out, out_width, n_max,
-                      minimal, s, sms, rl);
+                              int out_width, cudaStream_t s, int sms, bool pdl) {
+    return launch_src(ix, gamma_kind, pow2, KeySrc{bins, 2, 0, 0, 1, dyn_n, pdl}, out, out_width,
+                      n_max, /*minimal=*/0, s, sms, RemapList{nullptr, nullptr, nullptr, 0});
 }
 
 // ---------------------------------------------------------------------------

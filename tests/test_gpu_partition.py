@@ -86,3 +86,26 @@ def test_partitioned_skewed_streams_spill(ph, ref, pattern):
         out = idx.query(d_q, minimal=minimal, out_width=8)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), minimal
+
+
+@pytest.mark.parametrize("koff,ooff", [(1, 0), (0, 1), (1, 3), (2, 2)])
+def test_partitioned_unaligned_buffers(ph, ref, koff, ooff):
+    """Keys / outputs not 16-B aligned take the register-staged kernels instead of the
+    bulk-copy ones (pass A needs aligned keys, pass C's bulk store an aligned output)."""
+    from oracle.bindings import corpus_u64_np
+    n = 150_000
+    keys = corpus_u64_np(0, n, 64)
+    ptrh = ref.build_u64(keys, ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    nq = 2 * (1 << 20) + 5
+    q = corpus_u64_np(0, nq, 65)
+    q[:n] = keys
+    want = ri.query_u64(q, True, "loop", threads=THREADS)
+    base = torch.zeros(nq + koff, dtype=torch.int64, device="cuda")
+    base[koff:] = torch.from_numpy(q.view(np.int64)).cuda()
+    obuf = torch.zeros(nq + ooff, dtype=torch.int32, device="cuda")
+    out = obuf[ooff:]
+    idx.query(base[koff:], out=out, minimal=True, out_width=4)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32).astype(np.uint64), want)

@@ -257,9 +257,12 @@ constexpr int kBinTmaThreads = PH_BIN_TMA_THREADS;
 constexpr size_t kBinTmaSmem = 2 * kTileKeys * 8 + kBinTmaStage * (8 + 2);
 
 // Pass A, bulk-copy variant (u64 keys, 16-B aligned key array).
-template <int THREADS>
+// SRC = 1: keys are the k-mers of a packed sequence (seq_words, kbits), read with ordinary
+// loads (0.25 B per key); only the run stores use the bulk-copy engine.
+template <int THREADS, int SRC>
 __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
-    const uint64_t* __restrict__ keys, uint64_t n, uint64_t seed, uint32_t G, uint64_t cap,
+    const uint64_t* __restrict__ keys, uint64_t n, uint64_t seq_words, uint32_t kbits,
+    uint64_t seed, uint32_t G, uint64_t cap,
     unsigned long long* __restrict__ ctrl, uint64_t* __restrict__ runoff,
     uint16_t* __restrict__ runcnt, uint64_t* __restrict__ bins, uint16_t* __restrict__ bpos) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -274,7 +277,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
     constexpr int PER = kTileKeys / THREADS;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+    // tiles that arrive by bulk load (u64 keys only)
     const uint64_t nfull = n / kTileKeys;
+    auto bulk = [&](uint64_t t) { return SRC == 0 && t < nfull; };
     const uint64_t pol = policy_evict_first();
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -288,8 +293,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
         bulk_g2s(in + b * kTileKeys, keys + t * kTileKeys, kTileKeys * 8, &bar[b], pol);
     };
     if (tid == 0) {
-        if (blockIdx.x < nfull) issue(blockIdx.x, 0);
-        if (blockIdx.x + gridDim.x < nfull) issue(blockIdx.x + gridDim.x, 1);
+        if (bulk(blockIdx.x)) issue(blockIdx.x, 0);
+        if (bulk(blockIdx.x + gridDim.x)) issue(blockIdx.x + gridDim.x, 1);
     }
     uint32_t it = 0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
         const uint64_t t0 = t * kTileKeys;
         const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
         uint64_t k[PER];
-        if (t < nfull) {
+        if (bulk(t)) {
             mbar_wait(&bar[b], (it >> 1) & 1);
 #pragma unroll
             for (int j = 0; j < PER; j++) k[j] = in[b * kTileKeys + j * THREADS + tid];
@@ -305,7 +310,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
 #pragma unroll
             for (int j = 0; j < PER; j++) {
                 const uint32_t e = (uint32_t)j * THREADS + tid;
-                k[j] = e < valid ? __ldcs(keys + t0 + e) : 0;
+                if (SRC == 1)
+                    k[j] = e < valid ? part_kmer(keys, seq_words, t0 + e, kbits) : 0;
+                else
+                    k[j] = e < valid ? __ldcs(keys + t0 + e) : 0;
             }
         }
         uint32_t* c_ = cnt[b];
@@ -318,7 +326,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
             }
         }
         __syncthreads();  // #1: buffer b consumed, counts final
-        if (tid == 0 && t + 2 * (uint64_t)gridDim.x < nfull) issue(t + 2 * (uint64_t)gridDim.x, b);
+        if (tid == 0 && bulk(t + 2 * (uint64_t)gridDim.x)) issue(t + 2 * (uint64_t)gridDim.x, b);
         if (tid < kTmaGroups) cnt[b ^ 1][tid] = 0;  // next tile's counters
         // warp 0 (lane = group): the run reservation is issued first (its latency overlaps
         // the scan, barrier #2 and the staging)
@@ -581,15 +589,21 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
     cudaFuncSetAttribute(k_bin<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
     const uint64_t want = L.ntiles;
     const int grid_a = (int)(want < (uint64_t)sms * kBinCtas ? want : (uint64_t)sms * kBinCtas);
-    const bool tma = src_kind == 0 && G <= (uint32_t)kTmaGroups &&
-                     (reinterpret_cast<uintptr_t>(keys) & 15) == 0 &&
-                     !std::getenv("PH_GPU_NO_TMA");
+    const bool tma = G <= (uint32_t)kTmaGroups && !std::getenv("PH_GPU_NO_TMA") &&
+                     (src_kind == 1 || (reinterpret_cast<uintptr_t>(keys) & 15) == 0);
     if (tma) {
-        cudaFuncSetAttribute(k_bin_tma<kBinTmaThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kBinTmaSmem);
         const int grid_t = (int)(want < (uint64_t)sms * 2 ? want : (uint64_t)sms * 2);
-        k_bin_tma<kBinTmaThreads><<<grid_t, kBinTmaThreads, kBinTmaSmem, s>>>(
-            keys, n, ix.seed, G, L.cap, ctrl, runoff, runcnt, bins, bpos);
+        if (src_kind == 1) {
+            cudaFuncSetAttribute(k_bin_tma<kBinTmaThreads, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinTmaSmem);
+            k_bin_tma<kBinTmaThreads, 1><<<grid_t, kBinTmaThreads, kBinTmaSmem, s>>>(
+                keys, n, seq_words, kbits, ix.seed, G, L.cap, ctrl, runoff, runcnt, bins, bpos);
+        } else {
+            cudaFuncSetAttribute(k_bin_tma<kBinTmaThreads, 0>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinTmaSmem);
+            k_bin_tma<kBinTmaThreads, 0><<<grid_t, kBinTmaThreads, kBinTmaSmem, s>>>(
+                keys, n, 0, 0, ix.seed, G, L.cap, ctrl, runoff, runcnt, bins, bpos);
+        }
     } else if (src_kind == 1) {
         k_bin<1><<<grid_a, kBinThreads, smem_a, s>>>(keys, n, seq_words, kbits, ix.seed, G, L.cap,
                                                    ctrl, runoff, runcnt, bins, bpos);

@@ -42,6 +42,13 @@ namespace phg {
 #ifndef PH_L2_MINB
 #define PH_L2_MINB 8
 #endif
+// partitioned pass B (SRC = 2, non-minimal)
+#ifndef PH_B_KPT
+#define PH_B_KPT 4
+#endif
+#ifndef PH_B_MINB
+#define PH_B_MINB 8
+#endif
 
 // Warp-cooperative remap of the keys flagged in need[] (slot >= n).
 // Entries are ranked across (j, lane) with ballots; lane r of a round decodes
@@ -340,8 +347,8 @@ static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out
     const bool hotf = ix.hot_b < ix.B;
     if constexpr (SRC == 2) {  // binned entries: pilots of the current group are L2-resident
         if (hotf) return cudaErrorInvalidValue;  // the partitioned path needs the file order
-        return launch_u64_k<G, POW2, OutT, SRC, PH_L2_KPT, PH_L2_MINB, true, false>(ix, src, out, n, minimal, s,
-                                                                   sms, rl);
+        return launch_u64_k<G, POW2, OutT, SRC, PH_B_KPT, PH_B_MINB, false, false>(
+            ix, src, out, n, minimal, s, sms, rl);
     } else {
         const bool dram = hotf || g_regime == 2 ||
                           (g_regime == 0 && src.tuning == 0 && ix.P * ix.B > kDramRegimeBytes);

@@ -105,6 +105,10 @@ constexpr int kDefaultL2Flags = 0;
 
 }  // namespace
 
+namespace {
+struct Pipeline;
+}
+
 struct ph_gpu_index {
     int device = 0;
     int sms = 148;
@@ -115,6 +119,10 @@ struct ph_gpu_index {
     void* d_ef[3] = {nullptr, nullptr, nullptr};
     void* d_opt = nullptr;
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch for the deferred remap
+    // host-path pipelines (streams + staging buffers), reused across calls
+    mutable std::mutex pl_mu;
+    mutable std::vector<Pipeline*> pl_cache;
+    void (*pl_free)(ph_gpu_index*) = nullptr;  // frees pl_cache (defined with Pipeline)
 };
 
 namespace {
@@ -276,6 +284,7 @@ int apply_pilot_layout(ph_gpu_index* ix, const uint8_t* file, uint64_t hot_bytes
 void release(ph_gpu_index* ix) {
     if (!ix) return;
     DeviceGuard g(ix->device);
+    if (ix->pl_free) ix->pl_free(ix);
     cudaFree(ix->d_pilots);
     cudaFree(ix->d_remap);
     for (void* p : ix->d_ef) cudaFree(p);
@@ -623,6 +632,8 @@ struct Slot {
 
 struct Pipeline {
     Slot slot[kSlots];
+    size_t in_bytes = 0, off_bytes = 0, out_bytes = 0;
+    bool bounce = false;
     ~Pipeline() {
         for (Slot& s : slot) {
             if (s.s) cudaStreamSynchronize(s.s);
@@ -639,6 +650,10 @@ struct Pipeline {
 
 int alloc_pipeline(Pipeline& pl, size_t in_bytes, size_t off_bytes, size_t out_bytes,
                    bool bounce) {
+    pl.in_bytes = in_bytes;
+    pl.off_bytes = off_bytes;
+    pl.out_bytes = out_bytes;
+    pl.bounce = bounce;
     for (Slot& s : pl.slot) {
         PH_CUDA(cudaStreamCreateWithFlags(&s.s, cudaStreamNonBlocking));
         if (cudaMalloc(&s.d_in, in_bytes ? in_bytes : 1) != cudaSuccess ||
@@ -653,6 +668,60 @@ int alloc_pipeline(Pipeline& pl, size_t in_bytes, size_t off_bytes, size_t out_b
         }
     }
     return PH_OK;
+}
+
+// A pipeline borrowed from the index's cache for one host-path call (allocating streams
+// and staging buffers per call cost up to hundreds of ms when cudaFree synchronised the
+// device); concurrent callers get separate pipelines.
+struct PipelineLease {
+    const ph_gpu_index* ix = nullptr;
+    Pipeline* p = nullptr;
+    ~PipelineLease() {
+        if (!p) return;
+        for (Slot& s : p->slot)
+            if (s.s) cudaStreamSynchronize(s.s);
+        std::lock_guard<std::mutex> lk(ix->pl_mu);
+        if (ix->pl_cache.size() < 4) {
+            for (Slot& s : p->slot) s.pending = false;
+            ix->pl_cache.push_back(p);
+        } else {
+            delete p;
+        }
+    }
+    Pipeline& operator*() { return *p; }
+};
+
+void free_pipelines(ph_gpu_index* ix);
+
+int lease_pipeline(const ph_gpu_index* ix, size_t in_bytes, size_t off_bytes, size_t out_bytes,
+                   bool bounce, PipelineLease& L) {
+    L.ix = ix;
+    {
+        std::lock_guard<std::mutex> lk(ix->pl_mu);
+        for (size_t i = 0; i < ix->pl_cache.size(); i++) {
+            Pipeline* c = ix->pl_cache[i];
+            if (c->bounce == bounce && c->in_bytes >= in_bytes && c->off_bytes >= off_bytes &&
+                c->out_bytes >= out_bytes) {
+                ix->pl_cache.erase(ix->pl_cache.begin() + static_cast<long>(i));
+                L.p = c;
+                return PH_OK;
+            }
+        }
+    }
+    const_cast<ph_gpu_index*>(ix)->pl_free = free_pipelines;
+    auto* p = new Pipeline();
+    if (int rc = alloc_pipeline(*p, in_bytes, off_bytes, out_bytes, bounce)) {
+        delete p;
+        return rc;
+    }
+    L.p = p;
+    return PH_OK;
+}
+
+void free_pipelines(ph_gpu_index* ix) {
+    std::lock_guard<std::mutex> lk(ix->pl_mu);
+    for (Pipeline* p : ix->pl_cache) delete p;
+    ix->pl_cache.clear();
 }
 
 // Keys per pipeline chunk (default 8 Mi = 64 MiB of u64 keys); PH_GPU_CHUNK_KEYS overrides
@@ -685,8 +754,9 @@ int ph_gpu_index_stream_u64(const ph_gpu_index* ix, const uint64_t* h_keys, size
     }
     const size_t C = chunk_keys(n);
     const bool bounce = !(is_pinned_host(h_keys) && is_pinned_host(h_out));
-    Pipeline pl;
-    if (int rc = alloc_pipeline(pl, C * 8, 0, C * out_width, bounce)) return rc;
+    PipelineLease lease;
+    if (int rc = lease_pipeline(ix, C * 8, 0, C * out_width, bounce, lease)) return rc;
+    Pipeline& pl = *lease;
     auto* out_b = static_cast<uint8_t*>(h_out);
     auto drain = [&](Slot& s) -> int {
         if (!s.pending) return PH_OK;
@@ -751,8 +821,10 @@ int ph_gpu_index_stream_bytes(const ph_gpu_index* ix, const uint8_t* h_bytes,
     }
     const bool bounce = !(is_pinned_host(h_bytes) && is_pinned_host(h_offsets) &&
                           is_pinned_host(h_out));
-    Pipeline pl;
-    if (int rc = alloc_pipeline(pl, max_bytes, (C + 1) * 8, C * out_width, bounce)) return rc;
+    PipelineLease lease;
+    if (int rc = lease_pipeline(ix, max_bytes, (C + 1) * 8, C * out_width, bounce, lease))
+        return rc;
+    Pipeline& pl = *lease;
     auto* out_b = static_cast<uint8_t*>(h_out);
     auto drain = [&](Slot& s) -> int {
         if (!s.pending) return PH_OK;
@@ -841,8 +913,9 @@ int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uin
     const size_t C = chunk_keys(n) & ~size_t{31} ? chunk_keys(n) & ~size_t{31} : 32;  // windows
     const size_t max_words = (C + (size_t)k - 1 + 31) / 32 + 1;
     const bool bounce = !(is_pinned_host(h_seq) && is_pinned_host(h_out));
-    Pipeline pl;
-    if (int rc = alloc_pipeline(pl, max_words * 8, 0, C * out_width, bounce)) return rc;
+    PipelineLease lease;
+    if (int rc = lease_pipeline(ix, max_words * 8, 0, C * out_width, bounce, lease)) return rc;
+    Pipeline& pl = *lease;
     auto* out_b = static_cast<uint8_t*>(h_out);
     auto drain = [&](Slot& s) -> int {
         if (!s.pending) return PH_OK;

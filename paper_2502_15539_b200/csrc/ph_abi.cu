@@ -334,12 +334,10 @@ std::atomic<int> g_partition{0};  // 0 auto, 1 off, 2 force when the layout allo
 uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n, int out_width) {
     const int mode = g_partition.load();
     if (mode == 1 || !ix->pool || ix->dev.hot_b < ix->dev.B) return 0;  // needs file order
-    // pass B stores non-minimal slots in the output width
+    const uint64_t pb = ix->info.pilot_bytes;
+    // pass B stores non-minimal slots (minimal: remapped) in the output width
     if (out_width == PH_OUT_U32 && ix->info.parts * ix->info.slots_per_part > (uint64_t{1} << 32))
         return 0;
-    // pass C lists remap indices as u32
-    if (ix->info.parts * ix->info.slots_per_part - ix->info.n >= (uint64_t{1} << 32)) return 0;
-    const uint64_t pb = ix->info.pilot_bytes;
     if (mode == 0 && (pb <= (uint64_t{64} << 20) || n < pb / 2 || ix->dev.window_bytes))
         return 0;
     // pilot bytes per group (L2-resident); PH_GPU_PART_SLICE_MB overrides (tuning only)

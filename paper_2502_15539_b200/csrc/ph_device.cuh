@@ -259,4 +259,46 @@ __device__ __forceinline__ uint64_t remap_get_cold(const DevIndex& ix, uint64_t 
                           ix.ef_low_bits, idx);
 }
 
+// Warp-cooperative remap of the keys flagged in need[] (slot >= n).
+// Entries are ranked across (j, lane) with ballots; lane r of a round decodes
+// entry base+r; results return to their owners with shuffles.
+template <int KPT, class OutT>
+__device__ __forceinline__ void remap_tile(const DevIndex& ix, const bool (&need)[KPT],
+                                           uint64_t (&slot)[KPT]) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1;
+    unsigned m[KPT];
+    unsigned cum[KPT];
+    unsigned total = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+        m[j] = __ballot_sync(kFull, need[j]);
+        cum[j] = total;
+        total += __popc(m[j]);
+    }
+    if (total == 0) return;  // warp-uniform
+    for (unsigned base = 0; base < total; base += 32) {
+        const unsigned r = base + lane;
+        // gather the slot of entry r from its owner (j, src)
+        uint64_t my = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const unsigned cnt = __popc(m[j]);
+            const bool mine = r >= cum[j] && r < cum[j] + cnt;
+            const unsigned src = mine ? __fns(m[j], 0, (int)(r - cum[j]) + 1) : 0;
+            const uint64_t v = __shfl_sync(kFull, slot[j], src & 31);
+            if (mine) my = v;
+        }
+        uint64_t val = 0;
+        if (r < total) val = remap_get(ix, my - ix.n);
+        // hand results back
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const unsigned rr = cum[j] + __popc(m[j] & lt_mask);
+            const uint64_t v = __shfl_sync(kFull, val, (rr - base) & 31);
+            if (need[j] && rr >= base && rr < base + 32) slot[j] = v;
+        }
+    }
+}
+
 }  // namespace phg

@@ -78,14 +78,6 @@ cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2
                                    int minimal, cudaStream_t s, int sms, const RemapList& rl,
                                    bool l2_tuning);
 
-// Pass B of the partitioned path: bins[0, min(*dyn_n, n_max)) (device-side count), answered
-// into out[] at the same entry index with the L2-resident tuning.
-// Non-minimal slots only; pdl: launch as a programmatic dependent of the preceding kernel
-// (the kernels of consecutive groups do not depend on one another).
-cudaError_t launch_query_bins(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* bins,
-                              const unsigned long long* dyn_n, uint64_t n_max, void* out,
-                              int out_width, cudaStream_t s, int sms, bool pdl);
-
 // Partitioned path (ph_partition.cu). src_kind 0: keys = u64 keys; 1: keys = packed
 // sequence (seq_words, kbits), n = number of windows. scratch >= partition_scratch_bytes.
 uint64_t partition_scratch_bytes(uint64_t n, uint32_t G, int out_width);

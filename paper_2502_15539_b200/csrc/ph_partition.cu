@@ -42,9 +42,10 @@ constexpr uint32_t kTileKeys = kBinThreads * kBinPerThread;  // 4096 keys per ti
 constexpr int kBinCtas = 4;    // CTAs per SM (registers: 64 per thread)
 constexpr int kMaxGroups = 64;
 constexpr uint16_t kPadPos = 0xffff;  // position of a run's padding entry (never a tile position)
-// ctrl[]: per-group cursors [0, kMaxGroups), spill cursor
+// ctrl[]: per-group cursors [0, kMaxGroups), spill cursor, pass B's chunk counter
 constexpr int kCtrlSpill = kMaxGroups;
-constexpr int kCtrlWords = kMaxGroups + 1;
+constexpr int kCtrlWork = kMaxGroups + 1;
+constexpr int kCtrlWords = kMaxGroups + 2;
 
 // Group of a key: g = hi32(G * hi32(h)) for the hash h = C * (key ^ seed) (hash.hpp:27).
 // Monotone in h like part = hi(P * h) (bucket_fn.hpp:66-72), so each group's keys use a
@@ -238,6 +239,10 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// at most one bulk group (the most recent) may still be reading shared memory
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -247,8 +252,7 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 
 constexpr uint32_t kStageEntries = kTileKeys + 7 * kMaxGroups;  // runs padded to 8 entries
-constexpr int kTmaGroups = 32;
-constexpr uint32_t kRemapCap = 128;  // pass C: remap list entries per tile (k_remap_tiles)  // pass A's bulk-copy variant: G <= 32 (lane = group)
+constexpr int kTmaGroups = 32;  // pass A's bulk-copy variant: G <= 32 (lane = group)
 constexpr uint32_t kBinTmaStage = kTileKeys + 8 * kTmaGroups;  // (a multiple of 8)
 #ifndef PH_BIN_TMA_THREADS
 #define PH_BIN_TMA_THREADS 512
@@ -382,7 +386,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
 
 // Pass C, bulk-copy variant: the tile's runs (8-entry aligned) arrive by bulk loads two
 // tiles ahead (double-buffered), are scattered by position into the output tile in shared
-// memory, and the output tile leaves with one bulk store when `out` is 16-B aligned.
+// memory, and the output tile leaves with one bulk store when `out` is 16-B aligned. Warp 0
+// loads the run table of the tile it will issue next at the top of each iteration, so the
+// issue at the bottom does not wait on global loads while the other warps wait for it.
 template <class OutT>
 struct UnbinTma {
     static constexpr size_t kIn = (size_t)kStageEntries * (sizeof(OutT) + 2);  // one buffer
@@ -391,16 +397,12 @@ struct UnbinTma {
 
 template <class OutT>
 __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
-    const DevIndex ix, int minimal, uint64_t n, uint32_t G, const uint64_t* __restrict__ runoff,
+    uint64_t n, uint32_t G, const uint64_t* __restrict__ runoff,
     const uint16_t* __restrict__ runcnt, const uint16_t* __restrict__ bpos,
-    const OutT* __restrict__ slots, OutT* __restrict__ out, uint16_t* __restrict__ rl_pos,
-    uint32_t* __restrict__ rl_idx, uint32_t* __restrict__ rl_cnt) {
+    const OutT* __restrict__ slots, OutT* __restrict__ out) {
     extern __shared__ __align__(128) uint8_t smem[];
     OutT* stage = reinterpret_cast<OutT*>(smem + 2 * UnbinTma<OutT>::kIn);
     __shared__ __align__(8) uint64_t bar[2];
-    // remap_slot (index.hpp:98-100) of the tile's slots >= n: listed per tile for
-    // k_remap_tiles (the decode's dependent reads stay off this kernel's critical path)
-    __shared__ uint32_t nrem;
     __shared__ uint32_t mtot[2];             // per buffer: staged entries (runs padded to 8)
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
@@ -410,14 +412,22 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
         sv = reinterpret_cast<OutT*>(smem + b * UnbinTma<OutT>::kIn);
         pv = reinterpret_cast<uint16_t*>(sv + kStageEntries);
     };
-    // warp 0: bulk-load tile t's runs into buffer b
-    auto issue = [&](uint64_t t, int b) {
+    struct Meta {  // warp 0, lane l: the runs of groups 2l and 2l+1
+        uint32_t c0, c1;
+        uint64_t o0, o1;
+    };
+    auto meta = [&](uint64_t t) {
+        Meta m{0, 0, 0, 0};
         const uint32_t g0 = 2 * lane;
-        const uint32_t c0 = g0 < G ? __ldg(runcnt + t * G + g0) : 0;
-        const uint32_t c1 = g0 + 1 < G ? __ldg(runcnt + t * G + g0 + 1) : 0;
-        const uint64_t o0 = g0 < G ? __ldg(runoff + t * G + g0) : 0;
-        const uint64_t o1 = g0 + 1 < G ? __ldg(runoff + t * G + g0 + 1) : 0;
-        const uint32_t p0 = (c0 + 7) & ~7u, p1 = (c1 + 7) & ~7u;
+        if (t < ntiles) {
+            if (g0 < G) m.c0 = __ldg(runcnt + t * G + g0), m.o0 = __ldg(runoff + t * G + g0);
+            if (g0 + 1 < G) m.c1 = __ldg(runcnt + t * G + g0 + 1), m.o1 = __ldg(runoff + t * G + g0 + 1);
+        }
+        return m;
+    };
+    // warp 0: bulk-load a tile's runs (described by m) into buffer b
+    auto issue = [&](const Meta& m, int b) {
+        const uint32_t p0 = (m.c0 + 7) & ~7u, p1 = (m.c1 + 7) & ~7u;
         uint32_t x = p0 + p1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -435,12 +445,12 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
         uint16_t* pv;
         bufs(b, sv, pv);
         if (p0) {
-            bulk_g2s(sv + x, slots + o0, p0 * (uint32_t)sizeof(OutT), &bar[b], pol);
-            bulk_g2s(pv + x, bpos + o0, p0 * 2, &bar[b], pol);
+            bulk_g2s(sv + x, slots + m.o0, p0 * (uint32_t)sizeof(OutT), &bar[b], pol);
+            bulk_g2s(pv + x, bpos + m.o0, p0 * 2, &bar[b], pol);
         }
         if (p1) {
-            bulk_g2s(sv + x + p0, slots + o1, p1 * (uint32_t)sizeof(OutT), &bar[b], pol);
-            bulk_g2s(pv + x + p0, bpos + o1, p1 * 2, &bar[b], pol);
+            bulk_g2s(sv + x + p0, slots + m.o1, p1 * (uint32_t)sizeof(OutT), &bar[b], pol);
+            bulk_g2s(pv + x + p0, bpos + m.o1, p1 * 2, &bar[b], pol);
         }
     };
     if (tid == 0) {
@@ -450,19 +460,19 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
     }
     __syncthreads();
     if (warp == 0) {
-        if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
-        if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+        if (blockIdx.x < ntiles) issue(meta(blockIdx.x), 0);
+        if (blockIdx.x + gridDim.x < ntiles) issue(meta(blockIdx.x + gridDim.x), 1);
     }
     uint32_t it = 0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
         const int b = it & 1;
         const uint64_t t0 = t * kTileKeys;
         const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
+        const uint64_t tn = t + 2 * (uint64_t)gridDim.x;  // the tile buffer b serves next
+        Meta mn{0, 0, 0, 0};
+        if (warp == 0) mn = meta(tn);
         mbar_wait(&bar[b], (it >> 1) & 1);
-        if (tid == 0) {
-            bulk_wait_read();  // the previous output tile has left `stage`
-            nrem = 0;
-        }
+        if (tid == 0) bulk_wait_read();  // the previous output tile has left `stage`
         __syncthreads();
         OutT* sv;
         uint16_t* pv;
@@ -472,24 +482,10 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
 #pragma unroll 4
         for (uint32_t e = tid; e < total; e += kBinThreads) {
             const uint16_t p = pv[e];
-            const uint64_t v = sv[e];
-            if (p == kPadPos) continue;
-            if (minimal && v >= ix.n) {
-                const uint32_t r = atomicAdd(&nrem, 1u);
-                if (r < kRemapCap) {
-                    rl_pos[t * kRemapCap + r] = p;
-                    rl_idx[t * kRemapCap + r] = (uint32_t)(v - ix.n);
-                    stage[p] = 0;  // patched by k_remap_tiles
-                } else {
-                    stage[p] = (OutT)remap_get_cold(ix, v - ix.n);  // list full
-                }
-            } else {
-                stage[p] = (OutT)v;
-            }
+            if (p != kPadPos) stage[p] = sv[e];
         }
         fence_async_smem();
         __syncthreads();
-        if (minimal && tid == 0) rl_cnt[t] = min(nrem, kRemapCap);
         if (vec && valid == kTileKeys) {
             if (tid == 0) {
                 bulk_s2g(out + t0, stage, kTileKeys * (uint32_t)sizeof(OutT), pol);
@@ -498,33 +494,135 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
         } else {
             for (uint32_t e = tid; e < valid; e += kBinThreads) st_stream(out + t0 + e, stage[e]);
         }
-        if (warp == 0 && t + 2 * (uint64_t)gridDim.x < ntiles) issue(t + 2 * (uint64_t)gridDim.x, b);
+        if (warp == 0 && tn < ntiles) issue(mn, b);
     }
     if (tid == 0) bulk_wait_all();
 }
 
-// Pass C's remap lists: one warp per tile decodes its slots >= n and patches the outputs.
-template <class OutT>
-__global__ void __launch_bounds__(256) k_remap_tiles(const DevIndex ix, uint64_t ntiles,
-                                                     const uint16_t* __restrict__ rl_pos,
-                                                     const uint32_t* __restrict__ rl_idx,
-                                                     const uint32_t* __restrict__ rl_cnt,
-                                                     OutT* __restrict__ out) {
-    const unsigned lane = threadIdx.x & 31;
-    for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
-         t += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t c = rl_cnt[t];
-        for (uint32_t i = lane; i < c; i += 32)
-            out[t * kTileKeys + rl_pos[t * kRemapCap + i]] =
-                (OutT)remap_get(ix, rl_idx[t * kRemapCap + i]);
+// Pass B: the query arithmetic over the group regions (region r < G: group r, r == G: the
+// spill), non-minimal slots into slots[] at the same entry index (remap_slot happens in
+// pass C). CTAs claim 2048-entry chunks in order from a global counter, so the chunks in
+// flight always form one contiguous window (one or two regions): the current pilot slice
+// stays L2-resident. Dynamic claiming also keeps the pass balanced when it shares the SMs
+// with another chunk's pass A or C.
+constexpr int kQThreads = 256;
+constexpr int kQPer = 8;                              // keys per thread (4 pairs)
+constexpr uint32_t kQChunk = kQThreads * kQPer;       // 2048 entries per chunk
+#ifndef PH_QB_MINB
+#define PH_QB_MINB 4
+#endif
+
+template <int G, bool POW2, class OutT>
+__global__ void __launch_bounds__(kQThreads, PH_QB_MINB) k_query_regions(
+    const DevIndex ix, uint32_t NG, uint64_t cap, unsigned long long* __restrict__ ctrl,
+    const uint64_t* __restrict__ bins, OutT* __restrict__ slots, int minimal) {
+    __shared__ uint64_t cstart[kMaxGroups + 2];  // first chunk of each region
+    __shared__ uint64_t rend[kMaxGroups + 1];    // entry end of each region
+    __shared__ uint64_t claim[2];
+    const unsigned tid = threadIdx.x;
+    if (tid == 0) {
+        uint64_t c = 0;
+        for (uint32_t r = 0; r <= NG; r++) {
+            const uint64_t len = r < NG ? min((uint64_t)ctrl[r], cap) : (uint64_t)ctrl[kCtrlSpill];
+            cstart[r] = c;
+            rend[r] = (uint64_t)r * cap + len;
+            c += (len + kQChunk - 1) / kQChunk;
+        }
+        cstart[NG + 1] = c;
+        claim[0] = atomicAdd(ctrl + kCtrlWork, 1ull);
     }
+    __syncthreads();
+    const uint64_t nchunks = cstart[NG + 1];
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = ix.pilot_evict_normal ? policy_evict_normal() : policy_evict_last();
+    const uint32_t P32 = (uint32_t)ix.P, B32 = (uint32_t)ix.B, S32 = (uint32_t)ix.S;
+    uint32_t r = 0;
+    for (int k = 0;; k ^= 1) {
+        const uint64_t c = claim[k];
+        if (c >= nchunks) break;
+        if (tid == 0) claim[k ^ 1] = atomicAdd(ctrl + kCtrlWork, 1ull);  // next, in flight
+        while (c >= cstart[r + 1]) r++;
+        const uint64_t e0 = (uint64_t)r * cap + (c - cstart[r]) * kQChunk;
+        const uint64_t end = rend[r];  // region lengths are multiples of 8 entries
+        uint64_t h[kQPer];
+#pragma unroll
+        for (int q = 0; q < kQPer / 2; q++) {
+            const uint64_t e = e0 + ((uint64_t)q * kQThreads + tid) * 2;
+            h[2 * q] = h[2 * q + 1] = 0;
+            if (e < end)
+                asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                    : "=l"(h[2 * q]), "=l"(h[2 * q + 1])
+                    : "l"(bins + e), "l"(pol_stream));
+        }
+        uint32_t part[kQPer], pilot[kQPer];
+#pragma unroll
+        for (int j = 0; j < kQPer; j++) {
+            h[j] = kC * (h[j] ^ ix.seed);  // hash_int, hash.hpp:27
+            uint64_t x, unused;
+            part[j] = (uint32_t)mul32x64(P32, h[j], x);  // part_and_bucket, bucket_fn.hpp:66-72
+            const uint32_t bucket = (uint32_t)mul32x64(B32, gamma<G>(x, ix.opt_table), unused);
+            pilot[j] = ld_gather_u8(ix.pilots + ((uint64_t)part[j] * B32 + bucket), pol_keep);
+        }
+        uint64_t slot[kQPer];
+        bool need[kQPer];
+#pragma unroll
+        for (int j = 0; j < kQPer; j++) {  // slot_of, index.hpp:91-96
+            slot[j] = (uint64_t)part[j] * S32 + reduce<POW2>(ix, h[j] ^ hash_pilot(ix, pilot[j]));
+            const uint64_t e = e0 + ((uint64_t)(j >> 1) * kQThreads + tid) * 2 + (j & 1);
+            need[j] = minimal && slot[j] >= ix.n && e < end;
+        }
+        // remap_slot (index.hpp:98-100) for the ~1 % of slots >= n: ranked across the warp
+        // with ballots, one convergent round of CacheLineEF decodes (L2-resident table)
+        if (minimal) remap_tile<kQPer, OutT>(ix, need, slot);
+#pragma unroll
+        for (int q = 0; q < kQPer / 2; q++) {
+            const uint64_t e = e0 + ((uint64_t)q * kQThreads + tid) * 2;
+            if (e < end) {
+                if constexpr (sizeof(OutT) == 4)
+                    asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(slots + e),
+                                 "r"((uint32_t)slot[2 * q]), "r"((uint32_t)slot[2 * q + 1])
+                                 : "memory");
+                else
+                    asm volatile("st.global.cs.v2.u64 [%0], {%1,%2};" ::"l"(slots + e),
+                                 "l"(slot[2 * q]), "l"(slot[2 * q + 1])
+                                 : "memory");
+            }
+        }
+        __syncthreads();  // claim[k ^ 1] visible; claim[k] free for reuse
+    }
+}
+
+template <class OutT>
+static cudaError_t launch_regions(const DevIndex& ix, int gamma_kind, bool pow2, uint32_t G,
+                                  uint64_t cap, uint64_t nent, unsigned long long* ctrl,
+                                  const uint64_t* bins, OutT* slots, int minimal, cudaStream_t s,
+                                  int sms, int per_sm) {
+    const uint64_t chunks_max = nent / kQChunk + G + 2;
+    const int grid = (int)std::min<uint64_t>(chunks_max, (uint64_t)sms * per_sm);
+#define PH_CASE(GK)                                                                              \
+    case GK:                                                                                     \
+        if (pow2) k_query_regions<GK, true, OutT><<<grid, kQThreads, 0, s>>>(ix, G, cap, ctrl, bins, slots, minimal); \
+        else k_query_regions<GK, false, OutT><<<grid, kQThreads, 0, s>>>(ix, G, cap, ctrl, bins, slots, minimal);    \
+        break;
+    switch (gamma_kind) {
+        PH_CASE(0)
+        PH_CASE(1)
+        PH_CASE(2)
+        PH_CASE(3)
+        PH_CASE(4)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef PH_CASE
+    note_launch();
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 namespace {
 struct Layout {
     uint64_t cap, ntiles, nent;
-    uint64_t o_runoff, o_runcnt, o_bins, o_bpos, o_slots, o_rlpos, o_rlidx, o_rlcnt, total;
+    uint64_t o_runoff, o_runcnt, o_bins, o_bpos, o_slots, total;
 };
 Layout layout(uint64_t n, uint32_t G, int out_width) {
     auto al = [](uint64_t b) { return (b + 255) & ~uint64_t{255}; };
@@ -547,12 +645,6 @@ Layout layout(uint64_t n, uint32_t G, int out_width) {
     o += al(L.nent * 2);
     L.o_slots = o;
     o += al(L.nent * (uint64_t)out_width);
-    L.o_rlpos = o;
-    o += al(L.ntiles * kRemapCap * 2);
-    L.o_rlidx = o;
-    o += al(L.ntiles * kRemapCap * 4);
-    L.o_rlcnt = o;
-    o += al(L.ntiles * 4);
     L.total = o;
     return L;
 }
@@ -562,13 +654,25 @@ uint64_t partition_scratch_bytes(uint64_t n, uint32_t G, int out_width) {
     return layout(n, G, out_width).total;
 }
 
-cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool pow2,
+static int env_int(const char* name, int dflt) {  // launch-shape knobs (tools/synth_perf.py)
+    const char* e = std::getenv(name);
+    return e && std::atoi(e) > 0 ? std::atoi(e) : dflt;
+}
+
+cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool pow2,
                                      const uint64_t* keys, int src_kind, uint64_t seq_words,
                                      uint32_t kbits, void* out, int out_width, uint64_t n,
                                      int minimal, uint32_t G, void* scratch, cudaStream_t s,
                                      int sms) {
     if (n == 0) return cudaSuccess;
     if (G < 1 || G > (uint32_t)kMaxGroups) return cudaErrorInvalidValue;
+    // Pass B reads the pilots with evict_last: the L2 of each die then keeps its own copy of
+    // the far die's lines of the current slice (measured at config 3: L2 fabric requests
+    // 610M -> 101M, pass B 5.96 -> 4.84 ms); lines of earlier slices evict one another.
+    DevIndex ix = ix0;
+    ix.window_bytes = 0;
+    ix.pilot_evict_normal = env_int("PH_GPU_PB_NORMAL", 0) ? 1 : 0;
+    ix.cold_evict_first = 0;
     const Layout L = layout(n, G, out_width);
     uint8_t* base = static_cast<uint8_t*>(scratch);
     auto* ctrl = reinterpret_cast<unsigned long long*>(base);
@@ -577,12 +681,10 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
     auto* bins = reinterpret_cast<uint64_t*>(base + L.o_bins);
     auto* bpos = reinterpret_cast<uint16_t*>(base + L.o_bpos);
     void* slots = base + L.o_slots;
-    auto* rl_pos = reinterpret_cast<uint16_t*>(base + L.o_rlpos);
-    auto* rl_idx = reinterpret_cast<uint32_t*>(base + L.o_rlidx);
-    auto* rl_cnt = reinterpret_cast<uint32_t*>(base + L.o_rlcnt);
 
     cudaError_t e = cudaMemsetAsync(ctrl, 0, kCtrlWords * 8, s);
     if (e != cudaSuccess) return e;
+    // A: bin the keys by group
     const size_t smem_a = kTileKeys * (8 + 4);
     // (per device and cheap: set on every call)
     cudaFuncSetAttribute(k_bin<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
@@ -592,7 +694,8 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
     const bool tma = G <= (uint32_t)kTmaGroups && !std::getenv("PH_GPU_NO_TMA") &&
                      (src_kind == 1 || (reinterpret_cast<uintptr_t>(keys) & 15) == 0);
     if (tma) {
-        const int grid_t = (int)(want < (uint64_t)sms * 2 ? want : (uint64_t)sms * 2);
+        const uint64_t ctas = (uint64_t)sms * env_int("PH_GPU_PART_A_CTAS", 2);
+        const int grid_t = (int)(want < ctas ? want : ctas);
         if (src_kind == 1) {
             cudaFuncSetAttribute(k_bin_tma<kBinTmaThreads, 1>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinTmaSmem);
@@ -613,51 +716,27 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
     }
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    // B: the query kernel over the entries, one L2-sized pilot slice after another
-    // (no persisting window and evict_normal pilots: earlier slices must be evictable)
-    DevIndex ixb = ix;
-    ixb.window_bytes = 0;
-    ixb.pilot_evict_normal = 1;
-    ixb.cold_evict_first = 0;
-    // Pass B answers non-minimal slots (remap_slot happens in pass C), so its launches are
-    // independent of one another: each after the first is a programmatic dependent launch
-    // whose CTAs fill the SMs as the previous group's drain.
-    uint8_t* sl = static_cast<uint8_t*>(slots);
-    for (uint32_t g = 0; g <= G; g++) {  // g == G: the spill region
-        const uint64_t off = g * L.cap;
-        e = launch_query_bins(ixb, gamma_kind, pow2, bins + off, ctrl + (g < G ? g : kCtrlSpill),
-                              g < G ? L.cap : n, sl + off * out_width, out_width, s, sms,
-                              /*pdl=*/g > 0);
-        if (e != cudaSuccess) return e;
-    }
-    {
-        const size_t sm4 = UnbinTma<uint32_t>::kSmem, sm8 = UnbinTma<uint64_t>::kSmem;
-        cudaFuncSetAttribute(k_unbin_tma<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm4);
-        cudaFuncSetAttribute(k_unbin_tma<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm8);
-        const uint64_t ctas = (uint64_t)sms * (out_width == 4 ? 3 : 1);
-        const int grid_t = (int)(want < ctas ? want : ctas);
-        if (out_width == 4)
-            k_unbin_tma<uint32_t><<<grid_t, kBinThreads, sm4, s>>>(
-                ix, minimal, n, G, runoff, runcnt, bpos, static_cast<const uint32_t*>(slots),
-                static_cast<uint32_t*>(out), rl_pos, rl_idx, rl_cnt);
-        else
-            k_unbin_tma<uint64_t><<<grid_t, kBinThreads, sm8, s>>>(
-                ix, minimal, n, G, runoff, runcnt, bpos, static_cast<const uint64_t*>(slots),
-                static_cast<uint64_t*>(out), rl_pos, rl_idx, rl_cnt);
-        note_launch();
-        if (minimal) {
-            const uint64_t wb = (L.ntiles + 7) / 8;  // 8 warps (tiles) per block
-            const int gr = (int)(wb < (uint64_t)sms * 8 ? wb : (uint64_t)sms * 8);
-            if (out_width == 4)
-                k_remap_tiles<uint32_t><<<gr, 256, 0, s>>>(ix, L.ntiles, rl_pos, rl_idx, rl_cnt,
-                                                           static_cast<uint32_t*>(out));
-            else
-                k_remap_tiles<uint64_t><<<gr, 256, 0, s>>>(ix, L.ntiles, rl_pos, rl_idx, rl_cnt,
-                                                           static_cast<uint64_t*>(out));
-        }
-    }
+    // B: the query arithmetic (and remap_slot) over the group regions, one L2-resident
+    // pilot slice after another
+    const int b_per_sm = env_int("PH_GPU_PART_B_CTAS", 4);
+    e = out_width == 4
+            ? launch_regions(ix, gamma_kind, pow2, G, L.cap, L.nent, ctrl, bins,
+                             static_cast<uint32_t*>(slots), minimal, s, sms, b_per_sm)
+            : launch_regions(ix, gamma_kind, pow2, G, L.cap, L.nent, ctrl, bins,
+                             static_cast<uint64_t*>(slots), minimal, s, sms, b_per_sm);
+    if (e != cudaSuccess) return e;
+    // C: back to input order
+    const size_t sm4 = UnbinTma<uint32_t>::kSmem, sm8 = UnbinTma<uint64_t>::kSmem;
+    cudaFuncSetAttribute(k_unbin_tma<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+    cudaFuncSetAttribute(k_unbin_tma<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm8);
+    const uint64_t ctas = (uint64_t)sms * (out_width == 4 ? env_int("PH_GPU_PART_C_CTAS", 3) : 1);
+    const int grid_c = (int)(want < ctas ? want : ctas);
+    if (out_width == 4)
+        k_unbin_tma<uint32_t><<<grid_c, kBinThreads, sm4, s>>>(
+            n, G, runoff, runcnt, bpos, static_cast<const uint32_t*>(slots), static_cast<uint32_t*>(out));
+    else
+        k_unbin_tma<uint64_t><<<grid_c, kBinThreads, sm8, s>>>(
+            n, G, runoff, runcnt, bpos, static_cast<const uint64_t*>(slots), static_cast<uint64_t*>(out));
     note_launch();
     return cudaGetLastError();
 }

@@ -42,55 +42,6 @@ namespace phg {
 #ifndef PH_L2_MINB
 #define PH_L2_MINB 8
 #endif
-// partitioned pass B (SRC = 2, non-minimal)
-#ifndef PH_B_KPT
-#define PH_B_KPT 4
-#endif
-#ifndef PH_B_MINB
-#define PH_B_MINB 8
-#endif
-
-// Warp-cooperative remap of the keys flagged in need[] (slot >= n).
-// Entries are ranked across (j, lane) with ballots; lane r of a round decodes
-// entry base+r; results return to their owners with shuffles.
-template <int KPT, class OutT>
-__device__ __forceinline__ void remap_tile(const DevIndex& ix, const bool (&need)[KPT],
-                                           uint64_t (&slot)[KPT]) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1;
-    unsigned m[KPT];
-    unsigned cum[KPT];
-    unsigned total = 0;
-#pragma unroll
-    for (int j = 0; j < KPT; j++) {
-        m[j] = __ballot_sync(kFull, need[j]);
-        cum[j] = total;
-        total += __popc(m[j]);
-    }
-    if (total == 0) return;  // warp-uniform
-    for (unsigned base = 0; base < total; base += 32) {
-        const unsigned r = base + lane;
-        // gather the slot of entry r from its owner (j, src)
-        uint64_t my = 0;
-#pragma unroll
-        for (int j = 0; j < KPT; j++) {
-            const unsigned cnt = __popc(m[j]);
-            const bool mine = r >= cum[j] && r < cum[j] + cnt;
-            const unsigned src = mine ? __fns(m[j], 0, (int)(r - cum[j]) + 1) : 0;
-            const uint64_t v = __shfl_sync(kFull, slot[j], src & 31);
-            if (mine) my = v;
-        }
-        uint64_t val = 0;
-        if (r < total) val = remap_get(ix, my - ix.n);
-        // hand results back
-#pragma unroll
-        for (int j = 0; j < KPT; j++) {
-            const unsigned rr = cum[j] + __popc(m[j] & lt_mask);
-            const uint64_t v = __shfl_sync(kFull, val, (rr - base) & 31);
-            if (need[j] && rr >= base && rr < base + 32) slot[j] = v;
-        }
-    }
-}
 
 // k-mer key of window i of a 2-bit packed sequence (word w holds bases 32w..32w+31,
 // base 32w+t at bits 2(31-t), i.e. MSB-first): the k bases starting at i packed with the
@@ -169,14 +120,9 @@ __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex i
                                                    const uint64_t* __restrict__ keys,
                                                    OutT* __restrict__ out, uint64_t nkeys_arg,
                                                    int minimal, uint64_t seq_words,
-                                                   uint32_t kbits, const RemapList rl,
-                                                   const unsigned long long* __restrict__ dyn_n) {
+                                                   uint32_t kbits, const RemapList rl) {
     constexpr uint64_t kTile = 32ull * KPT;
-    // SRC = 2 (the partitioned path's pass B): u64 entries whose count (<= nkeys_arg) is
-    // only known on the device (written by pass A): no host synchronisation between passes.
-    const uint64_t nkeys = SRC == 2 ? min((uint64_t)*dyn_n, nkeys_arg) : nkeys_arg;
-    // a dependent launch of the next group may start filling SMs as this one's CTAs drain
-    if (SRC == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint64_t nkeys = nkeys_arg;
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -297,12 +243,10 @@ static int grid_for(K kernel, int threads, uint64_t work_items_per_block, uint64
 // 2-bit sequence (seq_words words, kbits = 2k).
 struct KeySrc {
     const uint64_t* ptr;
-    int kind;  // 0 = u64 array, 1 = k-mers, 2 = u64 array of device-side length *dyn_n
+    int kind;  // 0 = u64 array, 1 = k-mers
     uint64_t seq_words;
     uint32_t kbits;
-    int tuning;  // 0 = by pilot size, 1 = L2-resident tuning (the partitioned path's pass B)
-    const unsigned long long* dyn_n;
-    bool pdl;  // programmatic dependent launch (partitioned pass B)
+    int tuning;  // 0 = by pilot size, 1 = L2-resident tuning
 };
 
 // Two tunings of the same kernel, chosen per index by the pilot array's size
@@ -328,9 +272,8 @@ static cudaError_t launch_u64_k(const DevIndex& ix, const KeySrc& src, void* out
                            rl.cap / nlists >= 32)
                               ? rl
                               : RemapList{nullptr, nullptr, nullptr, 0};
-    cudaError_t e = launch_ex_pdl(ix, src.pdl, kern, blocks, threads, s, ix, src.ptr,
-                                  static_cast<OutT*>(out), n, minimal, src.seq_words, src.kbits,
-                                  use, src.dyn_n);
+    cudaError_t e = launch_ex(ix, kern, blocks, threads, s, ix, src.ptr, static_cast<OutT*>(out), n,
+                              minimal, src.seq_words, src.kbits, use);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e == cudaSuccess && use.idx) {
         k_remap_patch<OutT><<<(nlists + 7) / 8, 256, 0, s>>>(ix, use, nlists,
@@ -345,11 +288,7 @@ template <int G, bool POW2, class OutT, int SRC>
 static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out, uint64_t n,
                                 int minimal, cudaStream_t s, int sms, const RemapList& rl) {
     const bool hotf = ix.hot_b < ix.B;
-    if constexpr (SRC == 2) {  // binned entries: pilots of the current group are L2-resident
-        if (hotf) return cudaErrorInvalidValue;  // the partitioned path needs the file order
-        return launch_u64_k<G, POW2, OutT, SRC, PH_B_KPT, PH_B_MINB, false, false>(
-            ix, src, out, n, minimal, s, sms, rl);
-    } else {
+    {
         const bool dram = hotf || g_regime == 2 ||
                           (g_regime == 0 && src.tuning == 0 && ix.P * ix.B > kDramRegimeBytes);
         if (dram && hotf)
@@ -386,10 +325,6 @@ static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, con
                               void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                               int sms, const RemapList& rl) {
     if (n == 0) return cudaSuccess;
-    if (k.kind == 2)
-        return out_width == 4
-                   ? launch_u64_w<uint32_t, 2>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl)
-                   : launch_u64_w<uint64_t, 2>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl);
     if (k.kind == 1)
         return out_width == 4
                    ? launch_u64_w<uint32_t, 1>(ix, gamma_kind, pow2, k, out, n, minimal, s, sms, rl)
@@ -402,7 +337,7 @@ static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, con
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                              int sms, const RemapList& rl) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0, nullptr, false}, out, out_width, n, minimal, s,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0}, out, out_width, n, minimal, s,
                       sms, rl);
 }
 
@@ -411,7 +346,7 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                                cudaStream_t s, int sms, const RemapList& rl) {
     if (n_bases < (uint64_t)k) return cudaSuccess;
     const uint64_t n = n_bases - (uint64_t)k + 1;
-    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0, nullptr, false},
+    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0},
                       out, out_width, n, minimal, s, sms, rl);
 }
 
@@ -419,15 +354,8 @@ cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2
                                    const uint64_t* keys, void* out, int out_width, uint64_t n,
                                    int minimal, cudaStream_t s, int sms, const RemapList& rl,
                                    bool l2_tuning) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0, nullptr, false}, out,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0}, out,
                       out_width, n, minimal, s, sms, rl);
-}
-
-cudaError_t launch_query_bins(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* bins,
-                              const unsigned long long* dyn_n, uint64_t n_max, void* out,
-                              int out_width, cudaStream_t s, int sms, bool pdl) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{bins, 2, 0, 0, 1, dyn_n, pdl}, out, out_width,
-                      n_max, /*minimal=*/0, s, sms, RemapList{nullptr, nullptr, nullptr, 0});
 }
 
 // ---------------------------------------------------------------------------

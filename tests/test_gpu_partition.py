@@ -1,6 +1,7 @@
-"""GPU tests of the partitioned query path (ph_partition.cu): forced on for
+"""GPU tests of the partitioned query path (ph_bins.cu): forced on for
 small indexes (ph_gpu_set_partition(2)), its outputs must equal the reference's for u64
-keys and k-mers, u32/u64 outputs, minimal/non-minimal and ragged batch sizes."""
+keys and k-mers, u32/u64 outputs, minimal/non-minimal, every bucket function / reduce /
+remap encoding of the golden fixtures, and ragged batch sizes."""
 import ctypes as C
 import os
 
@@ -43,7 +44,38 @@ def test_partitioned_u64_vs_reference(ph, ref, nq):
             torch.cuda.synchronize()
             got = out.cpu().numpy().view(np.uint32 if width == 4 else np.uint64).astype(np.uint64)
             assert np.array_equal(got, want), (minimal, width)
-    assert ph.launch_count() - before >= 4 * 4  # bin/count/query/unbin per call
+    assert ph.launch_count() - before >= 3 * 4  # bin/gather/answer (+ remap lists) per call
+
+
+def _golden_u64():
+    from conftest import golden_names, load_golden
+    out = []
+    for name in golden_names():
+        ptrh, rec = load_golden(name)
+        if "queries" in rec:
+            out.append(name)
+    return out
+
+
+@pytest.mark.parametrize("name", _golden_u64())
+def test_partitioned_golden_fixtures(ph, name):
+    """Every u64 golden index (all five bucket functions, pow2 / fastmod S, plain32 /
+    CacheLineEF / Elias-Fano remaps, forced shapes) through the partitioned path."""
+    from conftest import load_golden
+    ptrh, rec = load_golden(name)
+    idx = ph.PtrHashIndex(ptrh)
+    q = np.array(rec["queries"], dtype=np.uint64)
+    q = np.concatenate([q] * 3)  # a few tiles, one partial
+    d_q = torch.from_numpy(q.view(np.int64)).cuda()
+    for minimal, key in ((True, "minimal"), (False, "nonminimal")):
+        want = np.concatenate([np.array(rec[key], dtype=np.uint64)] * 3)
+        for width in (4, 8):
+            if width == 4 and int(want.max()) >= 1 << 32:
+                continue
+            out = idx.query(d_q, minimal=minimal, out_width=width)
+            torch.cuda.synchronize()
+            got = out.cpu().numpy().view(np.uint32 if width == 4 else np.uint64).astype(np.uint64)
+            assert np.array_equal(got, want), (name, minimal, width)
 
 
 def test_partitioned_kmers_vs_reference(ph, ref, port):

@@ -23,6 +23,10 @@ bench.phb_gather_die.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only-mb", type=int, default=0, help="one footprint, one run per mode (ncu)")
+    args = ap.parse_args()
     s = torch.cuda.current_stream()
     sp = C.c_void_p(s.cuda_stream)
     chunk = 2048
@@ -60,7 +64,7 @@ def main():
     sink = torch.zeros(1, dtype=torch.int32, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     nl = 1 << 28
-    for mb in (32, 64, 96, 128, 160, 192, 256, 333):
+    for mb in ((args.only_mb,) if args.only_mb else (32, 64, 96, 128, 160, 192, 256, 333)):
         per = (mb << 20) // 2 // chunk
         n0, n1 = min(per, l0.numel()), min(per, l1.numel())
         r = {"footprint_mb": mb}
@@ -69,6 +73,8 @@ def main():
                 bench.phb_gather_die(buf.data_ptr(), l0.data_ptr(), n0, l1.data_ptr(), n1,
                                      smd.data_ptr(), chunk, nl, 7, mode, sink.data_ptr(), sp)
             run()
+            if args.only_mb:
+                continue
             best = 1e9
             for _ in range(3):
                 flush.zero_()

@@ -59,7 +59,7 @@ CONFIGS = {
     4: dict(kind="str", n=3 * 10**8, order="perm",
             desc="config4: n=3e8 distinct strings, len U[8,64], bytes 0x21-0x7E, one "
                  "concatenated buffer + u64 offsets, all keys in seeded shuffled order"),
-    5: dict(kind="kmer", n=10**9, k=31,
+    5: dict(kind="kmer", n=10**9, k=31, layout="file",
             desc="config5: every 31-mer of a seeded random ACGT sequence of 1e9+30 bases "
                  "(2-bit packed, first base in the MSBs), in sequence order; fused on-device "
                  "k-mer extraction"),
@@ -389,6 +389,8 @@ class KmerWork:
         self.ptrh = build_index_bytes(self.nq, dist, None, build=build, tag=f"kmer{k}")
         del kmers
         self.idx = ph_gpu.PtrHashIndex(self.ptrh, device=dist.local)
+        if cfg.get("layout") == "file":
+            self.idx.set_l2_policy(0, 2)  # file order: the partitioned path
         self.n = int(self.idx.info.n)
         self.bijective = self.n == self.nq  # no duplicate k-mer: outputs are a permutation
         self.pin_seq = torch.empty(nw, dtype=torch.int64).pin_memory()
@@ -729,11 +731,15 @@ def main():
     ap.add_argument("--verify", default="full", choices=["full", "sample", "none"])
     ap.add_argument("--cpu-sample", type=int, default=100_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="", choices=["", "file", "default"],
+                    help="override the config's pilot layout (file: partitioned path when large)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rules)")
         args.warmup = 3
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.layout:
+        cfg["layout"] = args.layout
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -324,11 +324,12 @@ struct DeferScratch {
 
 // Partitioned path (ph_partition.cu): for DRAM-sized pilot arrays and large
 // device-resident batches, keys are binned into G hash groups whose pilot slices (~12 MiB
-// each) stay L2-resident while the ordinary kernel answers them, then un-permuted.
+// each) stay L2-resident while pass B answers them group after group, then un-permuted.
 // It needs the file-order pilot layout without a persisting set-aside
 // (ph_gpu_index_set_l2_policy(index, 0, 2)); "auto" then uses it for batches of at least
-// pilot_bytes / 2 keys. Measured at config 3: 14.5 ms against 15.4 ms for the direct kernel
-// on the default hot-first layout (profiles/r01_partition_*.txt).
+// pilot_bytes / 2 keys (u64 keys and k-mer windows). Measured at config 3: 11.5 ms against
+// 15.3 ms for the direct kernel on the default hot-first layout; config 5 (k-mers): 13.3 ms
+// against 13.9 ms (profiles/r01_bench_config{3,5}.json, r01_synth_*).
 std::atomic<int> g_partition{0};  // 0 auto, 1 off, 2 force when the layout allows
 
 uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n, int out_width) {

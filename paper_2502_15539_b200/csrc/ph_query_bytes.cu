@@ -66,42 +66,46 @@ __device__ void fill_tables(AesTables& T) {
     }
 }
 
-// Lookup of T0[byte k of w] in this lane's copy with two ALU ops (shift + LOP3) and an LDS
-// whose base address folds into the instruction: byte offset ((w >> (8k-7)) & 0x7f80) | lane*4.
+// Lookup of T0[byte k of w] in this lane's copy: PRMT extracts byte k, LEA forms
+// byte*128 + (this lane's table base), LDS reads it -- three instructions per lookup.
+// tb = shared-window address of T.t0 plus lane*4.
 template <int K>
-__device__ __forceinline__ uint32_t tk(const AesTables& T, uint32_t w, uint32_t lane4) {
-    const uint32_t off = (K == 0 ? (w << 7) : (w >> (8 * K - 7))) & 0x7f80u;
-    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(T.t0) + (off | lane4));
+__device__ __forceinline__ uint32_t tk(uint32_t tb, uint32_t w) {
+    uint32_t byte, v;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(byte) : "r"(w), "n"(0x4440 + K));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"((byte << 7) + tb));
+    return v;
 }
 
 // state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
 // in-memory byte order of the __m128i in hash.cpp. AESENC = ShiftRows,
 // SubBytes, MixColumns, AddRoundKey (Intel semantics).
-__device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4],
-                                       const AesTables& T, uint32_t lane4) {
+__device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4], uint32_t tb) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        const uint32_t a0 = tk<0>(T, s[c], lane4);
-        const uint32_t a1 = tk<1>(T, s[(c + 1) & 3], lane4);
-        const uint32_t a2 = tk<2>(T, s[(c + 2) & 3], lane4);
-        const uint32_t a3 = tk<3>(T, s[(c + 3) & 3], lane4);
+        const uint32_t a0 = tk<0>(tb, s[c]);
+        const uint32_t a1 = tk<1>(tb, s[(c + 1) & 3]);
+        const uint32_t a2 = tk<2>(tb, s[(c + 2) & 3]);
+        const uint32_t a3 = tk<3>(tb, s[(c + 3) & 3]);
         o[c] = a0 ^ __funnelshift_l(a1, a1, 8) ^ __funnelshift_l(a2, a2, 16) ^
                __funnelshift_l(a3, a3, 24) ^ k[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
 }
-__device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)[4],
-                                           const AesTables& T, uint32_t lane4) {
+__device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)[4], uint32_t tb) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        o[c] = (((tk<0>(T, s[c], lane4) >> 8) & 0xff) |
-                (tk<1>(T, s[(c + 1) & 3], lane4) & 0xff00) |
-                ((tk<2>(T, s[(c + 2) & 3], lane4) << 8) & 0xff0000) |
-                ((tk<3>(T, s[(c + 3) & 3], lane4) << 16) & 0xff000000)) ^
-               k[c];
+        const uint32_t a0 = tk<0>(tb, s[c]), a1 = tk<1>(tb, s[(c + 1) & 3]);
+        const uint32_t a2 = tk<2>(tb, s[(c + 2) & 3]), a3 = tk<3>(tb, s[(c + 3) & 3]);
+        // S[x] is byte 1 of T0[x]: gather byte 1 of a0..a3 into bytes 0..3
+        uint32_t lo, hi, v;
+        asm("prmt.b32 %0, %1, %2, 0x0051;" : "=r"(lo) : "r"(a0), "r"(a1));  // bytes 0,1
+        asm("prmt.b32 %0, %1, %2, 0x5100;" : "=r"(hi) : "r"(a2), "r"(a3));  // bytes 2,3
+        asm("prmt.b32 %0, %1, %2, 0x7610;" : "=r"(v) : "r"(lo), "r"(hi));
+        o[c] = v ^ k[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
@@ -200,10 +204,12 @@ __device__ __forceinline__ void set128(uint32_t (&s)[4], uint64_t hi, uint64_t l
 }
 
 // aes_core + aes_hash, hash.cpp:114-153. k0/k1 come precomputed from the host (they depend
-// only on the seed, hash.cpp:116-119); the first round comes from the init table.
+// only on the seed, hash.cpp:116-119); the first round comes from the init table. The
+// zero-padded tail block (buf[15] ^= len - i) is the last iteration of the block loop, so a
+// key takes exactly ceil(len/16) absorbing rounds.
 __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
                          uint64_t seed, bool wide, const DevIndex& ix, const AesTables& T,
-                         uint32_t lane4, uint64_t& hi, uint64_t& lo) {
+                         uint32_t tb, uint64_t& hi, uint64_t& lo) {
     const uint32_t k0[4] = {ix.aes_k0[0], ix.aes_k0[1], ix.aes_k0[2], ix.aes_k0[3]};
     const uint32_t k1[4] = {ix.aes_k1[0], ix.aes_k1[1], ix.aes_k1[2], ix.aes_k1[3]};
     uint32_t s[4], w[4];
@@ -215,27 +221,20 @@ __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_
         s[3] = v.w;
     } else {
         set128(s, (uint64_t)len * kC, seed ^ (uint64_t)len);
-        aesenc(s, k0, T, lane4);
+        aesenc(s, k0, tb);
     }
-    uint32_t i = 0;
-    while (i + 16 <= len) {
-        load16(data, off + i, 16, w);
-#pragma unroll
-        for (int c = 0; c < 4; c++) s[c] ^= w[c];
-        aesenc(s, k1, T, lane4);
-        i += 16;
-    }
-    if (i < len) {
-        const uint32_t rem = len - i;
+    const uint32_t nblk = (len + 15) >> 4;
+    for (uint32_t b = 0; b < nblk; b++) {
+        const uint32_t i = b << 4, rem = len - i;
         load16(data, off + i, rem, w);
-        w[3] ^= rem << 24;  // buf[15] ^= len - i
+        if (rem < 16) w[3] ^= rem << 24;  // buf[15] ^= len - i
 #pragma unroll
         for (int c = 0; c < 4; c++) s[c] ^= w[c];
-        aesenc(s, k1, T, lane4);
+        aesenc(s, k1, tb);
     }
-    aesenc(s, k0, T, lane4);
-    aesenc(s, k1, T, lane4);
-    aesenclast(s, k0, T, lane4);
+    aesenc(s, k0, tb);
+    aesenc(s, k1, tb);
+    aesenclast(s, k0, tb);
     const uint64_t l = (uint64_t)s[0] | ((uint64_t)s[1] << 32);
     const uint64_t h = (uint64_t)s[2] | ((uint64_t)s[3] << 32);
     if (!wide) {
@@ -246,15 +245,28 @@ __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_
     }
 }
 
+// Keys per warp batch. A warp ranks its batch by block count ceil(len/16) (a counting sort
+// by ballots) and hashes the keys in that order, 32 at a time, so the lanes of a round run
+// the same number of rounds; outputs go back to their input positions.
+constexpr int kBatchPer = 4;
+constexpr int kBatch = 32 * kBatchPer;
+constexpr int kBytesThreads = 256;
+constexpr int kBytesWarps = kBytesThreads / 32;
+constexpr uint32_t kClasses = 8;  // block counts 0..6, and 7 for >= 7 blocks
+
 template <int G, bool POW2, class OutT>
-__global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
+__global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix,
                                                      const uint8_t* __restrict__ data,
                                                      const uint64_t* __restrict__ offsets,
                                                      uint64_t base_off, OutT* __restrict__ out, uint64_t nkeys,
                                                      int minimal) {
     __shared__ AesTables T;
+    __shared__ uint64_t s_off[kBytesWarps][kBatch + 1];
+    __shared__ uint8_t s_perm[kBytesWarps][kBatch];
     const int algo = ix.hash_algo;
-    const uint32_t lane4 = (threadIdx.x & 31) * 4;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1;
+    const uint32_t tb = (uint32_t)__cvta_generic_to_shared(T.t0) + lane * 4;
     if (algo == 1 || algo == 2) {
         fill_tables(T);
         __syncthreads();
@@ -262,54 +274,82 @@ __global__ void __launch_bounds__(256) k_query_bytes(const DevIndex ix,
         for (uint32_t len = threadIdx.x; len < kInitLens; len += blockDim.x) {
             uint32_t st[4];
             set128(st, (uint64_t)len * kC, ix.seed ^ (uint64_t)len);  // hash.cpp:120-122
-            aesenc(st, k0, T, lane4);
+            aesenc(st, k0, tb);
             T.init[len] = make_uint4(st[0], st[1], st[2], st[3]);
         }
         __syncthreads();
     }
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_cold = policy_evict_first();
-    // Grid-stride with whole-warp iterations so the remap ballot stays convergent.
-    const uint64_t nround = (nkeys + stride - 1) / stride;
-    for (uint64_t r = 0; r < nround; r++) {
-        const uint64_t i = r * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-        const bool valid = i < nkeys;
-        uint64_t hi = 0, lo = 0;
-        // offsets[i] per lane; offsets[i+1] from the next lane (one load per key)
-        const uint64_t oi = i <= nkeys ? __ldg(offsets + i) : 0;
-        uint64_t onext = __shfl_down_sync(kFull, oi, 1);
-        if ((threadIdx.x & 31) == 31 && valid) onext = __ldg(offsets + i + 1);
-        if (valid) {
-            const uint64_t o0 = oi - base_off, o1 = onext - base_off;
-            const uint32_t len = (uint32_t)(o1 - o0);
-            if (algo == 1 || algo == 2) {
-                aes_hash(data, o0, len, ix.seed, algo == 2, ix, T, lane4, hi, lo);
-            } else if (algo == 4) {
-                hi = portable_hash64(data, o0, len, ix.seed ^ kP3);
-                lo = portable_hash64(data, o0, len, mix64(ix.seed) + kGolden);
-            } else {
-                hi = lo = portable_hash64(data, o0, len, ix.seed);
+    const uint64_t nwarps = (uint64_t)gridDim.x * kBytesWarps;
+    uint64_t* so = s_off[warp];
+    uint8_t* sp = s_perm[warp];
+    for (uint64_t base = (blockIdx.x * (uint64_t)kBytesWarps + warp) * kBatch; base < nkeys;
+         base += nwarps * kBatch) {
+        const uint32_t cnt = (uint32_t)(nkeys - base < (uint64_t)kBatch ? nkeys - base : kBatch);
+        // offsets[base .. base+cnt] into shared memory (coalesced)
+#pragma unroll
+        for (int r = 0; r < kBatchPer; r++) {
+            const uint32_t e = r * 32 + lane;
+            if (e <= cnt) so[e] = __ldg(offsets + base + e);
+        }
+        if (lane == 0 && cnt == kBatch) so[kBatch] = __ldg(offsets + base + kBatch);
+        __syncwarp();
+        // counting sort of the batch by block count (invalid slots last)
+        uint32_t cls[kBatchPer];
+#pragma unroll
+        for (int r = 0; r < kBatchPer; r++) {
+            const uint32_t e = r * 32 + lane;
+            const uint64_t len = e < cnt ? so[e + 1] - so[e] : 0;
+            const uint64_t nb = (len + 15) >> 4;
+            cls[r] = e < cnt ? (nb < kClasses - 1 ? (uint32_t)nb : kClasses - 1) : kClasses;
+        }
+        uint32_t run = 0;
+        for (uint32_t c = 0; c <= kClasses; c++) {
+#pragma unroll
+            for (int r = 0; r < kBatchPer; r++) {
+                const unsigned m = __ballot_sync(kFull, cls[r] == c);
+                if (cls[r] == c) sp[run + __popc(m & lt)] = (uint8_t)(r * 32 + lane);
+                run += __popc(m);
             }
         }
-        const uint64_t part = mulhi(ix.P, hi);
-        const uint64_t bucket = mulhi(ix.B, gamma<G>(ix.P * hi, ix.opt_table));
-        const bool hot = bucket < ix.hot_b;
-        const uint32_t pilot =
-            valid ? ld_gather_u8(ix.pilots + pilot_offset(ix, part, bucket),
-                                 (hot || !ix.cold_evict_first) ? pol_keep : pol_cold)
-                  : 0;
-        uint64_t slot[1] = {part * ix.S + reduce<POW2>(ix, lo ^ hash_pilot(ix, pilot))};
-        if (minimal) {
-            const bool need = valid && slot[0] >= ix.n;
-            if (__any_sync(kFull, need)) {
-                // rare path: every flagged lane decodes (one convergent round per warp)
-                uint64_t v = 0;
-                if (need) v = remap_get(ix, slot[0] - ix.n);
-                if (need) slot[0] = v;
+        __syncwarp();
+        for (int q = 0; q < kBatchPer; q++) {
+            const uint32_t e = sp[q * 32 + lane];
+            const bool valid = e < cnt;
+            uint64_t hi = 0, lo = 0;
+            if (valid) {
+                const uint64_t o0 = so[e] - base_off, o1 = so[e + 1] - base_off;
+                const uint32_t len = (uint32_t)(o1 - o0);
+                if (algo == 1 || algo == 2) {
+                    aes_hash(data, o0, len, ix.seed, algo == 2, ix, T, tb, hi, lo);
+                } else if (algo == 4) {
+                    hi = portable_hash64(data, o0, len, ix.seed ^ kP3);
+                    lo = portable_hash64(data, o0, len, mix64(ix.seed) + kGolden);
+                } else {
+                    hi = lo = portable_hash64(data, o0, len, ix.seed);
+                }
             }
+            const uint64_t part = mulhi(ix.P, hi);
+            const uint64_t bucket = mulhi(ix.B, gamma<G>(ix.P * hi, ix.opt_table));
+            const bool hot = bucket < ix.hot_b;
+            const uint32_t pilot =
+                valid ? ld_gather_u8(ix.pilots + pilot_offset(ix, part, bucket),
+                                     (hot || !ix.cold_evict_first) ? pol_keep : pol_cold)
+                      : 0;
+            uint64_t slot = part * ix.S + reduce<POW2>(ix, lo ^ hash_pilot(ix, pilot));
+            if (minimal) {
+                const bool need = valid && slot >= ix.n;
+                if (__any_sync(kFull, need)) {
+                    // rare path: every flagged lane decodes (one convergent round per warp)
+                    uint64_t v = 0;
+                    if (need) v = remap_get(ix, slot - ix.n);
+                    if (need) slot = v;
+                }
+            }
+            if (valid) st_stream(out + base + e, slot);
         }
-        if (valid) st_stream(out + i, slot[0]);
+        __syncwarp();  // s_off / s_perm are rewritten by the next batch
     }
 }
 
@@ -318,13 +358,14 @@ static cudaError_t launch_b(const DevIndex& ix, const uint8_t* d, const uint64_t
                             uint64_t bo, void* out, uint64_t n, int minimal, cudaStream_t s, int sms) {
     auto kern = k_query_bytes<G, POW2, OutT>;
     int bps = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0) != cudaSuccess || bps <= 0)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kBytesThreads, 0) != cudaSuccess ||
+        bps <= 0)
         bps = 1;
-    const uint64_t want = (n + 255) / 256;
+    const uint64_t want = (n + (uint64_t)kBatch * kBytesWarps - 1) / ((uint64_t)kBatch * kBytesWarps);
     const uint64_t cap = (uint64_t)sms * bps;
     const int blocks = (int)(want < cap ? want : cap);
     const cudaError_t e =
-        launch_ex(ix, kern, blocks, 256, s, ix, d, o, bo, static_cast<OutT*>(out), n, minimal);
+        launch_ex(ix, kern, blocks, kBytesThreads, s, ix, d, o, bo, static_cast<OutT*>(out), n, minimal);
     note_launch();
     return e;
 }

@@ -36,9 +36,12 @@
 
 namespace phg {
 
+#ifndef PH_TILE_KEYS
+#define PH_TILE_KEYS 4096
+#endif
 constexpr int kBinThreads = 256;
-constexpr int kBinPerThread = 16;
-constexpr uint32_t kTileKeys = kBinThreads * kBinPerThread;  // 4096 keys per tile
+constexpr uint32_t kTileKeys = PH_TILE_KEYS;  // keys per tile (positions are u16)
+constexpr int kBinPerThread = kTileKeys / kBinThreads;
 constexpr int kBinCtas = 4;    // CTAs per SM (registers: 64 per thread)
 constexpr int kMaxGroups = 64;
 constexpr uint16_t kPadPos = 0xffff;  // position of a run's padding entry (never a tile position)
@@ -253,6 +256,7 @@ __device__ __forceinline__ void fence_mbar_init() {
 
 constexpr uint32_t kStageEntries = kTileKeys + 7 * kMaxGroups;  // runs padded to 8 entries
 constexpr int kTmaGroups = 32;  // pass A's bulk-copy variant: G <= 32 (lane = group)
+
 constexpr uint32_t kBinTmaStage = kTileKeys + 8 * kTmaGroups;  // (a multiple of 8)
 #ifndef PH_BIN_TMA_THREADS
 #define PH_BIN_TMA_THREADS 512

@@ -341,8 +341,11 @@ uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n, int out_width) {
         return 0;
     if (mode == 0 && (pb <= (uint64_t{64} << 20) || n < pb / 2 || ix->dev.window_bytes))
         return 0;
-    // pilot bytes per group (L2-resident); PH_GPU_PART_SLICE_MB overrides (tuning only)
-    uint64_t slice = uint64_t{12} << 20;
+    // pilot bytes per group (L2-resident with pass B's evict_last loads). Fewer, larger
+    // groups mean longer runs, i.e. fewer bulk copies and atomics in passes A and C; the
+    // sweep at config 3 (profiles/r01_partition_slice_sweep.txt) has its optimum at 32 MiB
+    // (G = 11: 10.2 ms; 12 MiB 11.6 ms, 64 MiB 10.6 ms). PH_GPU_PART_SLICE_MB overrides.
+    uint64_t slice = uint64_t{32} << 20;
     if (const char* e = std::getenv("PH_GPU_PART_SLICE_MB"))
         if (std::atoll(e) > 0) slice = static_cast<uint64_t>(std::atoll(e)) << 20;
     uint64_t G = (pb + slice - 1) / slice;

@@ -348,6 +348,8 @@ uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n, int out_width) {
     uint64_t slice = uint64_t{32} << 20;
     if (const char* e = std::getenv("PH_GPU_PART_SLICE_MB"))
         if (std::atoll(e) > 0) slice = static_cast<uint64_t>(std::atoll(e)) << 20;
+    if (const char* e = std::getenv("PH_GPU_PART_SLICE_KB"))  // (tests: many groups)
+        if (std::atoll(e) > 0) slice = static_cast<uint64_t>(std::atoll(e)) << 10;
     uint64_t G = (pb + slice - 1) / slice;
     if (G < 2) G = 2;
     return G > 64 ? 0 : static_cast<uint32_t>(G);

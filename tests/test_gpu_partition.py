@@ -141,3 +141,24 @@ def test_partitioned_unaligned_buffers(ph, ref, koff, ooff):
     idx.query(base[koff:], out=out, minimal=True, out_width=4)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint32).astype(np.uint64), want)
+
+
+@pytest.mark.parametrize("slice_kb,nq", [(40, 1_000_003), (24, 2 * (1 << 20) + 11), (12, 1_000_003)])
+def test_partitioned_many_groups(ph, ref, slice_kb, nq, monkeypatch):
+    """Small pilot slices force many groups: ~17 and ~28 (bulk-copy pass A, lane = group)
+    and ~56 (> 32: the register-staged pass A)."""
+    from oracle.bindings import corpus_u64_np
+    n = 2_000_000
+    keys = corpus_u64_np(0, n, 66)
+    ptrh = ref.build_u64(keys, ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    q = corpus_u64_np(0, nq, 67)
+    q[: min(nq, n) // 2] = keys[: min(nq, n) // 2]
+    d_q = torch.from_numpy(q.view(np.int64)).cuda()
+    monkeypatch.setenv("PH_GPU_PART_SLICE_KB", str(slice_kb))
+    for minimal in (True, False):
+        want = ri.query_u64(q, minimal, "loop", threads=THREADS)
+        out = idx.query(d_q, minimal=minimal, out_width=4)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32).astype(np.uint64), want), minimal

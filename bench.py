@@ -495,10 +495,17 @@ def run_ours(args, cfg):
     pil = torch.empty(int(info.pilot_bytes), dtype=torch.uint8, device="cuda")
     sink = torch.zeros(1, dtype=torch.int32, device="cuda")
     nl = 1 << 28
-    g_ms = time_ms(lambda: bench.phb_gather(C.c_void_p(pil.data_ptr()), C.c_uint64(pil.numel()),
-                                            C.c_uint64(nl), C.c_uint64(1), 8, 8,
-                                            C.c_void_p(sink.data_ptr()), sp))
-    r_gather = nl / g_ms / 1e6  # G sectors/s
+
+    def gather_rate(nbytes):  # G random 1-byte loads (sectors) / s over an nbytes buffer
+        g_ms = time_ms(lambda: bench.phb_gather(C.c_void_p(pil.data_ptr()), C.c_uint64(nbytes),
+                                                C.c_uint64(nl), C.c_uint64(1), 8, 8,
+                                                C.c_void_p(sink.data_ptr()), sp))
+        return nl / g_ms / 1e6
+
+    r_gather = gather_rate(pil.numel())
+    # the partitioned path's pass B gathers from one L2-resident slice (32 MiB) at a time
+    slice_bytes = min(pil.numel(), 32 << 20)
+    r_gather_slice = gather_rate(slice_bytes)
     del pil
 
     # ---- timed region: value ----
@@ -531,6 +538,19 @@ def run_ours(args, cfg):
     ms_nm, _ = timed(False)
     total_ms = dist.max(sum(ms_min))
     total_nm = dist.max(sum(ms_nm))
+
+    # ---- per-pass times of the partitioned path (separate loop: events between passes) ----
+    passes = None
+    if cfg.get("layout") == "file" and info.pilot_bytes > (64 << 20):
+        ph_gpu.set_pass_timing(True)
+        for _ in range(args.steps):
+            flush.zero_()
+            W.query(out, True, stream.cuda_stream)
+        torch.cuda.synchronize()
+        sums, calls = ph_gpu.pass_times()
+        ph_gpu.set_pass_timing(False)
+        if calls:
+            passes = [dist.max(x / calls) for x in sums]
 
     # ---- timed region: e2e through the public host API ----
     for _ in range(2):
@@ -575,6 +595,7 @@ def run_ours(args, cfg):
     cpu = None
     if dist.rank == 0 and N == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(W, args)
+    bin_bytes = (W.stream_bytes - 4.0) + 10.0  # keys (or packed bases) in; key + position out
     res = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -616,6 +637,27 @@ def run_ours(args, cfg):
                             "copy_gbs": round(bw_copy, 1),
                             "r_gather_gsectors_s": round(r_gather, 3),
                             "gather_buffer_bytes": int(info.pilot_bytes)},
+        "partition_passes": None if passes is None else {
+            "method": "CUDA events around the three passes on the query stream "
+                      "(ph_gpu_set_pass_timing), mean over a separate loop of the same steps",
+            "bin": {"kernel": "k_bin_tma", "ms": round(passes[0], 4),
+                    "bound": "hbm", "algorithmic_bytes_per_key": round(bin_bytes, 3),
+                    "achieved_gbs": round(nq * bin_bytes / passes[0] / 1e6, 1),
+                    "frac": round(nq * bin_bytes / passes[0] / 1e6 / peak, 4)},
+            "query": {"kernel": "k_query_regions", "ms": round(passes[1], 4),
+                      "bound": "L1TEX wavefronts / L2 tag lookups of the random pilot gather "
+                               "(one 32-B sector per key from an L2-resident slice)",
+                      "gathers_gsectors_s": round(nq * sectors / passes[1] / 1e6, 2),
+                      "peak_gsectors_s": round(r_gather_slice, 2),
+                      "peak_source": f"live k_gather microbenchmark over {slice_bytes >> 20} MiB",
+                      "frac": round(nq * sectors / passes[1] / 1e6 / r_gather_slice, 4),
+                      "stream_bytes_per_key": 12.0},
+            "unbin": {"kernel": "k_unbin_tma", "ms": round(passes[2], 4),
+                      "bound": "hbm", "algorithmic_bytes_per_key": 10.0,
+                      "achieved_gbs": round(nq * 10.0 / passes[2] / 1e6, 1),
+                      "frac": round(nq * 10.0 / passes[2] / 1e6 / peak, 4)},
+            "dominant": ["bin", "query", "unbin"][max(range(3), key=lambda i: passes[i])],
+        },
         "gate": gate,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,

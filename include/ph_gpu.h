@@ -137,6 +137,12 @@ int ph_gpu_set_defer_min(uint64_t min_keys);
  * 0 = automatic (DRAM-sized pilot arrays, batches >= pilot_bytes/2 keys), 1 = never,
  * 2 = whenever the layout allows. Results are identical. */
 int ph_gpu_set_partition(int mode);
+/* Profiling aid (one host thread): when on, partitioned-path calls record CUDA events around
+ * their three passes (bin, query, unbin; up to 256 calls). ph_gpu_pass_times waits for the
+ * recorded calls and returns the summed milliseconds of each pass and the call count;
+ * ph_gpu_set_pass_timing resets the record. */
+int ph_gpu_set_pass_timing(int on);
+int ph_gpu_pass_times(double* ms_sums3, int* calls);
 /* Kernel tuning for u64/k-mer queries: 0 = automatic (by pilot bytes vs L2), 1 = the
  * L2-resident tuning, 2 = the DRAM-bound tuning. Tuning/bench knob. */
 int ph_gpu_set_regime(int regime);

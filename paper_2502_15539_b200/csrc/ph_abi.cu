@@ -410,6 +410,15 @@ extern "C" {
 
 const char* ph_gpu_last_error(void) { return g_err.c_str(); }
 uint64_t ph_gpu_launch_count(void) { return phg::launch_count(); }
+int ph_gpu_set_pass_timing(int on) {
+    phg::set_pass_timing(on != 0);
+    return PH_OK;
+}
+int ph_gpu_pass_times(double* ms_sums3, int* calls) {
+    if (!ms_sums3 || !calls) return fail(PH_E_INVALID, "null argument");
+    return phg::pass_times(ms_sums3, calls) == 0 ? PH_OK
+                                                 : fail(PH_E_CUDA, "pass timing events failed");
+}
 int ph_gpu_set_partition(int mode) {
     if (mode < 0 || mode > 2) return fail(PH_E_INVALID, "partition mode must be 0, 1 or 2");
     g_partition.store(mode);

@@ -87,6 +87,10 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
                                      int minimal, uint32_t G, void* scratch, cudaStream_t s,
                                      int sms);
 
+// Per-pass event timing of the partitioned path (A, B, C), summed over the timed calls.
+void set_pass_timing(bool on);
+int pass_times(double* ms_sums, int* calls);
+
 cudaError_t launch_relayout(const uint8_t* src, uint8_t* dst, uint64_t P, uint64_t B, uint64_t H,
                             cudaStream_t s);
 cudaError_t launch_verify(const void* out, int out_width, uint64_t count, uint64_t n,

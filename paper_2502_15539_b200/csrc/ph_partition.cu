@@ -654,6 +654,45 @@ Layout layout(uint64_t n, uint32_t G, int out_width) {
 }
 }  // namespace
 
+// Optional per-pass timing (ph_gpu_set_pass_timing / ph_gpu_pass_times): cudaEvents on the
+// call's stream around passes A, B and C of up to kTimedCalls calls. A profiling aid for
+// bench.py's per-pass roofline; one host thread at a time.
+namespace {
+constexpr int kTimedCalls = 256;
+struct PassTiming {
+    bool on = false;
+    int calls = 0;
+    cudaEvent_t ev[kTimedCalls][4] = {};
+} g_pt;
+void pt_record(int k, cudaStream_t s) {
+    if (!g_pt.on || g_pt.calls >= kTimedCalls) return;
+    cudaEvent_t& e = g_pt.ev[g_pt.calls][k];
+    if (!e) cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    if (k == 3) g_pt.calls++;
+}
+}  // namespace
+
+void set_pass_timing(bool on) {
+    g_pt.on = on;
+    g_pt.calls = 0;
+}
+
+int pass_times(double* ms_sums, int* calls) {
+    ms_sums[0] = ms_sums[1] = ms_sums[2] = 0;
+    for (int c = 0; c < g_pt.calls; c++) {
+        cudaEvent_t* e = g_pt.ev[c];
+        if (cudaEventSynchronize(e[3]) != cudaSuccess) return -1;
+        for (int k = 0; k < 3; k++) {
+            float ms = 0;
+            if (cudaEventElapsedTime(&ms, e[k], e[k + 1]) != cudaSuccess) return -1;
+            ms_sums[k] += ms;
+        }
+    }
+    *calls = g_pt.calls;
+    return 0;
+}
+
 uint64_t partition_scratch_bytes(uint64_t n, uint32_t G, int out_width) {
     return layout(n, G, out_width).total;
 }
@@ -686,6 +725,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
     auto* bpos = reinterpret_cast<uint16_t*>(base + L.o_bpos);
     void* slots = base + L.o_slots;
 
+    pt_record(0, s);
     cudaError_t e = cudaMemsetAsync(ctrl, 0, kCtrlWords * 8, s);
     if (e != cudaSuccess) return e;
     // A: bin the keys by group
@@ -722,6 +762,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // B: the query arithmetic (and remap_slot) over the group regions, one L2-resident
     // pilot slice after another
+    pt_record(1, s);
     const int b_per_sm = env_int("PH_GPU_PART_B_CTAS", 4);
     e = out_width == 4
             ? launch_regions(ix, gamma_kind, pow2, G, L.cap, L.nent, ctrl, bins,
@@ -729,6 +770,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
             : launch_regions(ix, gamma_kind, pow2, G, L.cap, L.nent, ctrl, bins,
                              static_cast<uint64_t*>(slots), minimal, s, sms, b_per_sm);
     if (e != cudaSuccess) return e;
+    pt_record(2, s);
     // C: back to input order
     const size_t sm4 = UnbinTma<uint32_t>::kSmem, sm8 = UnbinTma<uint64_t>::kSmem;
     cudaFuncSetAttribute(k_unbin_tma<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
@@ -742,6 +784,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
         k_unbin_tma<uint64_t><<<grid_c, kBinThreads, sm8, s>>>(
             n, G, runoff, runcnt, bpos, static_cast<const uint64_t*>(slots), static_cast<uint64_t*>(out));
     note_launch();
+    pt_record(3, s);
     return cudaGetLastError();
 }
 

@@ -114,6 +114,23 @@ def set_regime(regime: int):
     _check(_L.ph_gpu_set_regime(regime))
 
 
+_L.ph_gpu_set_pass_timing.argtypes = [C.c_int]
+_L.ph_gpu_pass_times.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int)]
+
+
+def set_pass_timing(on: bool):
+    """Record CUDA events around the partitioned path's passes (profiling aid)."""
+    _check(_L.ph_gpu_set_pass_timing(1 if on else 0))
+
+
+def pass_times():
+    """(summed ms of bin, query, unbin passes, number of timed calls) since set_pass_timing."""
+    ms = (C.c_double * 3)()
+    calls = C.c_int(0)
+    _check(_L.ph_gpu_pass_times(ms, C.byref(calls)))
+    return [ms[0], ms[1], ms[2]], calls.value
+
+
 def _is_torch(x):
     return type(x).__module__.startswith("torch")
 

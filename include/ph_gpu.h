@@ -148,13 +148,16 @@ int ph_gpu_pass_times(double* ms_sums3, int* calls);
 int ph_gpu_set_regime(int regime);
 /* Override the bulk-kernel launch shape (0 = automatic). For tuning/bench. */
 int ph_gpu_set_launch(int threads_per_block, int blocks_per_sm);
-/* Pilot layout and L2 policy (default: hot_bytes = 64 MiB, flags = 0). Pilot arrays larger
- * than hot_bytes are laid out hot-first: the first hot_bytes/P buckets of every part form a
- * contiguous region covered by a persisting L2 access-policy window (this sets the
- * context's cudaLimitPersistingL2CacheSize). hot_bytes = 0 or flag 2 (no window) keeps the
- * file order and releases the device-wide persisting set-aside (the partitioned path needs
- * both). flag 1: cold-region loads use L2::evict_first. Results are unaffected. Do not call
- * while queries on `index` are in flight. */
+/* Pilot layout and L2 policy. Default: pilot arrays of at most 64 MiB keep the file order
+ * under a persisting L2 window over all of it (hot_bytes = 64 MiB, flags = 0); larger ones
+ * keep the file order without a window (hot_bytes = 0, flags = 2), so large batches take the
+ * partitioned path. Pilot arrays larger than a nonzero hot_bytes are laid out hot-first: the
+ * first hot_bytes/P buckets of every part form a contiguous region covered by a persisting
+ * L2 access-policy window (this sets the context's cudaLimitPersistingL2CacheSize).
+ * hot_bytes = 0 or flag 2 (no window) keeps the file order and releases the device-wide
+ * persisting set-aside (the partitioned path needs both). flag 1: cold-region loads use
+ * L2::evict_first. Results are unaffected. Do not call while queries on `index` are in
+ * flight. */
 int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flags);
 
 #ifdef __cplusplus

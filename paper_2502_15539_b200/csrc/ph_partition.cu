@@ -4,17 +4,19 @@
 // every direct query pays a DRAM row activation for its 1-byte pilot read (~57 G/s over
 // 333 MB). This path turns those random DRAM reads into streaming passes plus L2-resident
 // random reads. Keys are binned by hash group g = hi(G * h): group g's keys only use parts
-// [gP/G, (g+1)P/G], a contiguous ~P*B/G-byte slice of the pilots that fits in the L2.
+// [gP/G, (g+1)P/G], a contiguous ~P*B/G-byte slice (32 MiB by default) of the pilots.
 //
-//   A  bin     per 4096-key tile: ranks by group in shared memory, one global atomicAdd
-//              per (tile, group) to reserve a run in that group's region, then the runs are
-//              written from shared memory with coalesced stores: entry = (key, position in
-//              the tile as u16). Run (offset, length) -> runoff/runcnt[tile][g].
-//   B  query   the ordinary query kernel (L2-resident tuning), one launch per group region
-//              (so the warps of a launch only touch that group's pilot slice), then one
-//              over the spill; answers into slots[] at the same entry index.
-//   C  unbin   per tile: the G runs' (position, slot) pairs are scattered into a shared
-//              memory tile, which is then written to out[] with coalesced stores.
+//   A  bin     per 4096-key tile (bulk-copied into shared memory): ranks by group with
+//              shared-memory atomics, one global atomicAdd per (tile, group) reserves a run
+//              in that group's region, and each run leaves shared memory as bulk stores:
+//              entry = (key, position in the tile as u16); run (offset, length) ->
+//              runoff/runcnt[tile][g].
+//   B  query   one persistent kernel; CTAs claim chunks of the group regions in order from
+//              a global counter, so the chunks in flight stay within one or two slices,
+//              which stay L2-resident (evict_last). Full query arithmetic incl. remap_slot;
+//              answers into slots[] at the same entry index.
+//   C  unbin   per tile: the G runs' (position, slot) pairs are bulk-loaded, scattered into
+//              a shared-memory tile and written to out[] with one bulk store.
 //
 // Group regions have a fixed capacity (n/G plus 16 sigma plus a tile); a run that does not
 // fit goes to a spill region sized for the worst case (any distribution of queries, e.g.
@@ -510,7 +512,10 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
 // stays L2-resident. Dynamic claiming also keeps the pass balanced when it shares the SMs
 // with another chunk's pass A or C.
 constexpr int kQThreads = 256;
-constexpr int kQPer = 8;                              // keys per thread (4 pairs)
+#ifndef PH_QB_PER
+#define PH_QB_PER 8
+#endif
+constexpr int kQPer = PH_QB_PER;                      // keys per thread (pairs)
 constexpr uint32_t kQChunk = kQThreads * kQPer;       // 2048 entries per chunk
 #ifndef PH_QB_MINB
 #define PH_QB_MINB 4

@@ -355,6 +355,6 @@ def test_pilot_layouts_bitexact(ph, ref, hot_bytes, flags):
                                   ri.query_u64(q, True, "loop", threads=THREADS))
         finally:
             ph.set_partition(0)
-    idx.set_l2_policy(64 << 20, 0)  # back to the default
+    idx.set_l2_policy(64 << 20, 0)  # back to the default of an L2-sized pilot array
     assert np.array_equal(gpu_query(idx, keys, True, 8),
                           ri.query_u64(keys, True, "loop", threads=THREADS))

@@ -162,3 +162,24 @@ def test_partitioned_many_groups(ph, ref, slice_kb, nq, monkeypatch):
         out = idx.query(d_q, minimal=minimal, out_width=4)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32).astype(np.uint64), want), minimal
+
+
+def test_pass_timing_records_three_passes(ph, ref):
+    """ph_gpu_set_pass_timing / ph_gpu_pass_times: one partitioned call records positive
+    times for the bin, query and unbin passes; direct-path calls record nothing."""
+    from oracle.bindings import corpus_u64_np
+    n = 300_000
+    keys = corpus_u64_np(0, n, 68)
+    idx = ph.PtrHashIndex(ref.build_u64(keys, ref.params("default", lambda_=(30, 10))))
+    d_q = torch.from_numpy(keys.view(np.int64)).cuda()
+    ph.set_pass_timing(True)
+    try:
+        idx.query(d_q, minimal=True, out_width=4)
+        ms, calls = ph.pass_times()
+        assert calls == 1 and all(t > 0 for t in ms), (ms, calls)
+        ph.set_partition(1)  # direct kernel: no pass events
+        idx.query(d_q, minimal=True, out_width=4)
+        ph.set_partition(2)
+        assert ph.pass_times()[1] == 1
+    finally:
+        ph.set_pass_timing(False)

@@ -132,8 +132,8 @@ int ph_gpu_set_defer_min(uint64_t min_keys);
 /* Partitioned path for device-resident u64 / k-mer batches: keys are
  * binned by hash group so each group's pilot slice stays L2-resident, answered, then
  * restored to input order. Needs the file-order pilot layout without a persisting window
- * (ph_gpu_index_set_l2_policy(index, 0, 2)) and ~28 B/key of stream-ordered scratch from
- * the index's pool (falls back to the direct kernel if it cannot be had).
+ * (the default for pilot arrays > 64 MiB) and ~30 B/key of stream-ordered scratch from the
+ * index's pool (falls back to the direct kernel if it cannot be had).
  * 0 = automatic (DRAM-sized pilot arrays, batches >= pilot_bytes/2 keys), 1 = never,
  * 2 = whenever the layout allows. Results are identical. */
 int ph_gpu_set_partition(int mode);

@@ -111,6 +111,31 @@ __device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)
     for (int c = 0; c < 4; c++) s[c] = o[c];
 }
 
+// Bytes [sh, sh+16) of the 32-byte concatenation lo|hi as 4 LE words, zero from byte
+// `avail` on (avail < 16: the zero-padded tail block): a two-level select on the word
+// shift and one funnel shift per word.
+__device__ __forceinline__ void realign16(const uint4& lo, const uint4& hi, uint32_t sh,
+                                          uint32_t avail, uint32_t (&w)[4]) {
+    const uint32_t r[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t s2[7], a[5];
+    const bool w2 = sh & 8, w1 = sh & 4;
+#pragma unroll
+    for (int t = 0; t < 7; t++) s2[t] = w2 ? (t + 2 < 8 ? r[t + 2] : 0) : r[t];
+#pragma unroll
+    for (int t = 0; t < 5; t++) a[t] = w1 ? s2[t + 1] : s2[t];
+    const uint32_t rb = (sh & 3) * 8;
+#pragma unroll
+    for (int t = 0; t < 4; t++) w[t] = __funnelshift_r(a[t], a[t + 1], rb);
+    if (avail < 16) {
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int keep = (int)avail - 4 * t;  // bytes to keep in word t
+            if (keep <= 0) w[t] = 0;
+            else if (keep < 4) w[t] &= (1u << (8 * keep)) - 1;
+        }
+    }
+}
+
 // Loads min(avail,16) bytes at base+off as 4 LE words, zero past `avail`, with at most
 // two aligned 16-byte loads. Only aligned 16-byte granules that hold at least one
 // requested byte are read, so no access leaves the granules covering the key.
@@ -122,26 +147,7 @@ __device__ __forceinline__ void load16(const uint8_t* __restrict__ base, uint64_
     const uint32_t nb = avail < 16 ? avail : 16;
     const uint4 lo = __ldg(p);
     const uint4 hi = (sh + nb > 16) ? __ldg(p + 1) : make_uint4(0, 0, 0, 0);
-    uint32_t r[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    if (sh & 8) {
-#pragma unroll
-        for (int t = 0; t < 6; t++) r[t] = r[t + 2];
-    }
-    if (sh & 4) {
-#pragma unroll
-        for (int t = 0; t < 7; t++) r[t] = r[t + 1];
-    }
-    const uint32_t rb = (sh & 3) * 8;
-#pragma unroll
-    for (int t = 0; t < 4; t++) w[t] = __funnelshift_r(r[t], r[t + 1], rb);
-    if (avail < 16) {
-#pragma unroll
-        for (int t = 0; t < 4; t++) {
-            const int keep = (int)avail - 4 * t;  // bytes to keep in word t
-            if (keep <= 0) w[t] = 0;
-            else if (keep < 4) w[t] &= (1u << (8 * keep)) - 1;
-        }
-    }
+    realign16(lo, hi, sh, avail, w);
 }
 
 __device__ __forceinline__ uint64_t mum(uint64_t a, uint64_t b) {  // hash.cpp:53-56
@@ -223,14 +229,27 @@ __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_
         set128(s, (uint64_t)len * kC, seed ^ (uint64_t)len);
         aesenc(s, k0, tb);
     }
+    // The key's bytes arrive as aligned 16-byte granules g0..gl, prefetched one block ahead
+    // (block b needs granules b and b+1; granule b+2 is loaded while block b is hashed).
+    // No granule past gl is read, i.e. no access leaves the granules covering the key.
     const uint32_t nblk = (len + 15) >> 4;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + off);
+    const uint4* gp = reinterpret_cast<const uint4*>(a0 & ~uintptr_t{15});
+    const uint32_t sh = (uint32_t)(a0 & 15);
+    const uint32_t gl = len ? (sh + len - 1) >> 4 : 0;
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    uint4 cur = nblk ? __ldg(gp) : zero;
+    uint4 nxt = gl >= 1 ? __ldg(gp + 1) : zero;
     for (uint32_t b = 0; b < nblk; b++) {
-        const uint32_t i = b << 4, rem = len - i;
-        load16(data, off + i, rem, w);
+        const uint4 nn = b + 2 <= gl ? __ldg(gp + b + 2) : zero;  // prefetch
+        const uint32_t rem = len - (b << 4);
+        realign16(cur, nxt, sh, rem, w);
         if (rem < 16) w[3] ^= rem << 24;  // buf[15] ^= len - i
 #pragma unroll
         for (int c = 0; c < 4; c++) s[c] ^= w[c];
         aesenc(s, k1, tb);
+        cur = nxt;
+        nxt = nn;
     }
     aesenc(s, k0, tb);
     aesenc(s, k1, tb);
@@ -304,8 +323,14 @@ __global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix
             const uint64_t nb = (len + 15) >> 4;
             cls[r] = e < cnt ? (nb < kClasses - 1 ? (uint32_t)nb : kClasses - 1) : kClasses;
         }
+        uint32_t present = 0;  // classes that occur in the batch (usually 4-5 of 9)
+#pragma unroll
+        for (int r = 0; r < kBatchPer; r++) present |= 1u << cls[r];
+        present = __reduce_or_sync(kFull, present);
         uint32_t run = 0;
-        for (uint32_t c = 0; c <= kClasses; c++) {
+        while (present) {
+            const uint32_t c = __ffs(present) - 1;
+            present &= present - 1;
 #pragma unroll
             for (int r = 0; r < kBatchPer; r++) {
                 const unsigned m = __ballot_sync(kFull, cls[r] == c);

@@ -116,6 +116,19 @@ int ph_gpu_index_u64(const ph_gpu_index* index, uint64_t key, int minimal, uint6
 int ph_gpu_index_bytes(const ph_gpu_index* index, const uint8_t* key, size_t len, int minimal,
                        uint64_t* out);
 
+/* ---- construction assist (not the query path) ---- */
+/* The data-parallel phases of one u64 build attempt (construction.cpp:28-60): hash_all
+ * (construction.cpp:98-111), scatter_to_parts (engine.hpp:412-474) and each part's
+ * std::sort + duplicate check (engine.hpp:505-518), on `device`, synchronous. d_hashes[n]
+ * receives the hashes C*(key^seed) in part-major order with every part sorted (the array the
+ * reference's pilot search consumes), d_offsets[parts+1] the part boundaries. *status: 0 ok,
+ * 1 = a part holds more than slots_per_part keys (the reference's kOversubscribed), 2 = equal
+ * hashes (kDuplicateHashes). Its ~9 B/key of device scratch stays cached in a per-device
+ * memory pool for later calls. */
+int ph_gpu_build_prepare_u64(const uint64_t* d_keys, size_t n, uint64_t parts,
+                             uint64_t slots_per_part, uint64_t seed, int device,
+                             uint64_t* d_hashes, uint64_t* d_offsets, int* status);
+
 /* ---- verification ---- */
 /* verify_bijection (proj/tools/ptrhash.cpp:186-210) on `device`, synchronous: counts the
  * outputs >= n and the repeated outputs among d_out[0..count) (u32 or u64). */

@@ -88,6 +88,8 @@ class Ref:
         L.ref_clef_encode.argtypes = [u64p, C.c_size_t, u8p]
         L.ref_clef_get.argtypes = [u8p, C.c_size_t]
         L.ref_clef_get.restype = C.c_uint64
+        L.ref_build_prepare_u64.argtypes = [u64p, C.c_size_t, C.c_uint64, C.c_uint64,
+                                            C.c_uint64, C.c_uint, u64p, u64p]
         L.ref_hw_threads.restype = C.c_uint
 
     # ---- params / shape ----
@@ -187,6 +189,19 @@ class Ref:
     def clef_get(self, block: bytes, i: int) -> int:
         arr = (C.c_uint8 * 64).from_buffer_copy(block)
         return self.L.ref_clef_get(C.cast(arr, u8p), i)
+
+    # ---- construction front phases (hash_all, scatter_to_parts, per-part sort) ----
+    def build_prepare_u64(self, keys, P: int, S: int, seed: int, threads: int = 0):
+        """The reference's own hash_all + scatter_to_parts + per-part std::sort
+        (construction.cpp:98-111, engine.hpp:412-518): (hashes, offsets, status) with status
+        0 ok, 1 kOversubscribed, 2 kDuplicateHashes."""
+        k = np.ascontiguousarray(keys, dtype=np.uint64)
+        h = np.empty(k.size, dtype=np.uint64)
+        off = np.empty(P + 1, dtype=np.uint64)
+        st = self.L.ref_build_prepare_u64(_ptr(k), k.size, P, S, seed, threads, _ptr(h), _ptr(off))
+        if st < 0:
+            raise RuntimeError(self.err())
+        return h, off, st
 
 
 class RefIndex:
@@ -463,6 +478,25 @@ def corpus_u64_np(start: int, count: int, gen_seed: int) -> np.ndarray:
     i = np.arange(start + 1, start + count + 1, dtype=np.uint64)
     with np.errstate(over="ignore"):
         return mix64_np(np.uint64(gen_seed) + i * _GOLD)
+
+
+def build_prepare_u64_np(keys: np.ndarray, P: int, S: int, seed: int):
+    """Numpy restatement of one u64 build attempt's front phases (the oracle for
+    ph_gpu_build_prepare_u64): hash_all H64{C*(key^seed)} (construction.cpp:98-111,
+    hash.hpp:27); part = mul_hi(P, h) (engine.hpp:429) and the part-major arrangement with
+    kOversubscribed when a part holds more than S keys (engine.hpp:412-474); each part sorted
+    with kDuplicateHashes on equal neighbours (engine.hpp:505-518). part is monotone in h, so
+    one global sort gives the part-major, per-part-sorted array."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = np.sort(np.uint64(0x517CC1B727220A95) * (k ^ np.uint64(seed)))
+        # mul_hi(P, h) for P < 2^32: (P*h_hi + (P*h_lo >> 32)) >> 32 without overflow
+        part = (np.uint64(P) * (h >> np.uint64(32)) +
+                ((np.uint64(P) * (h & np.uint64(0xFFFFFFFF))) >> np.uint64(32))) >> np.uint64(32)
+    off = np.searchsorted(part, np.arange(P + 1, dtype=np.uint64), side="left").astype(np.uint64)
+    if (np.diff(off) > S).any():
+        return h, off, 1
+    return h, off, 2 if (h.size > 1 and (h[1:] == h[:-1]).any()) else 0
 
 
 def string_corpus(n: int, seed: int, lo=8, hi=64):

@@ -12,7 +12,9 @@
 //   threaded slices              proj/tools/ptrhash.cpp:486-512 (chunk = n/T + 1)
 //   hash/gamma/reduce/clef prims hash.hpp:27-32, hash.cpp:159, bucket_fn.hpp:49-72,
 //                                reduce.hpp:27-77, cacheline_ef.cpp:33-65
+//   build-attempt front phases   construction.cpp:28-60,98-111; engine.hpp:412-518
 
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -28,6 +30,8 @@
 #include "ptrhash/index.hpp"
 #include "ptrhash/serde.hpp"
 #include "ptrhash/sharding.hpp"
+#include "ptrhash/kernels.hpp"
+#include "engine.hpp"  // proj/src: detail::H64, detail::scatter_to_parts
 
 using namespace ptrhash;
 
@@ -303,5 +307,44 @@ uint64_t ref_clef_get(const uint8_t* block64, size_t i) {
     return clef_get(b, i);
 }
 uint64_t ref_corpus_u64(uint64_t i, uint64_t gen_seed) { return corpus_u64(i, gen_seed); }
+
+// The data-parallel front of one u64 build attempt, with the reference's own code:
+// hash_all (construction.cpp:98-111: kernels::active_ops().hash_u64 into detail::H64),
+// detail::scatter_to_parts (engine.hpp:412-474) and each part's std::sort + duplicate check
+// (engine.hpp:505-518). Returns 0 ok, 1 kOversubscribed, 2 kDuplicateHashes, -1 error;
+// hashes_out[n] part-major and sorted, offsets_out[P+1].
+int ref_build_prepare_u64(const uint64_t* keys, size_t n, uint64_t P, uint64_t S, uint64_t seed,
+                          unsigned threads, uint64_t* hashes_out, uint64_t* offsets_out) {
+    return guarded([&] {
+        Shape shape;
+        shape.n = n;
+        shape.parts = P;
+        shape.slots_per_part = S;
+        std::vector<detail::H64> h(n);
+        kernels::active_ops().hash_u64(keys, n, seed, reinterpret_cast<uint64_t*>(h.data()));
+        std::vector<uint64_t> offsets;
+        const auto f = detail::scatter_to_parts<detail::H64>(
+            shape, h, 0, P, detail::effective_threads(threads), offsets);
+        if (f == detail::AttemptFail::kOversubscribed) return 1;
+        // parts sorted in parallel, as build_parts does (engine.hpp:484-518)
+        std::atomic<uint64_t> next{0};
+        std::atomic<int> status{0};
+        std::vector<std::thread> workers;
+        const unsigned t = detail::effective_threads(threads);
+        for (unsigned w = 0; w < t; w++)
+            workers.emplace_back([&] {
+                for (uint64_t p; (p = next.fetch_add(1)) < P;) {
+                    auto b = h.begin() + offsets[p], e = h.begin() + offsets[p + 1];
+                    std::sort(b, e);
+                    for (auto it = b; it != e && it + 1 != e; ++it)
+                        if (*it == *(it + 1)) status = 2;
+                }
+            });
+        for (auto& th : workers) th.join();
+        std::memcpy(hashes_out, h.data(), n * 8);
+        std::memcpy(offsets_out, offsets.data(), (P + 1) * 8);
+        return status.load();
+    });
+}
 
 }  // extern "C"

@@ -84,7 +84,7 @@ def build_variants(defs, log=None, force=False):
     outs = []
     for name, flags in defs.items():
         out = build_lib(os.path.join("variants", f"libph_gpu_{name}.so"),
-                        ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_abi.cu"], extra=flags, log=log,
+                        ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_build.cu", "ph_abi.cu"], extra=flags, log=log,
                         force=force)
         outs.append(out)
     return outs
@@ -95,7 +95,7 @@ def main(force=False):
     os.makedirs(os.path.dirname(log), exist_ok=True)
     open(log, "w").close()
     libs = [
-        build_lib("libph_gpu.so", ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_abi.cu"], log=log,
+        build_lib("libph_gpu.so", ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_build.cu", "ph_abi.cu"], log=log,
                   force=force),
         build_lib("libph_bench.so", ["ph_bench.cu"], log=log, force=force),
     ]

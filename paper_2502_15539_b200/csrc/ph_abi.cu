@@ -1072,4 +1072,19 @@ int ph_gpu_verify_bijection(const void* d_out, size_t count, int out_width, uint
     return PH_OK;
 }
 
+int ph_gpu_build_prepare_u64(const uint64_t* d_keys, size_t n, uint64_t parts,
+                             uint64_t slots_per_part, uint64_t seed, int device,
+                             uint64_t* d_hashes, uint64_t* d_offsets, int* status) {
+    if ((!d_keys && n) || (!d_hashes && n) || !d_offsets || !status)
+        return fail(PH_E_INVALID, "null argument");
+    if (parts == 0 || slots_per_part == 0) return fail(PH_E_INVALID, "degenerate shape");
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const cudaError_t e = phg::build_prepare_u64(d_keys, n, parts, slots_per_part, seed, d_hashes,
+                                                 d_offsets, status, nullptr, sms);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "build_prepare_u64");
+}
+
 }  // extern "C"

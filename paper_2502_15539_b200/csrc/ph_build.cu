@@ -1,0 +1,131 @@
+// ph_build.cu — device assist for the construction phases that precede the pilot search
+// (SURVEY §8f-3). Not part of the query path; the pilot search stays on the CPU.
+//
+// For u64 keys one build attempt of the reference (construction.cpp:28-60, run_attempt)
+// starts with three data-parallel phases:
+//   hash_all          construction.cpp:98-111   H64{C * (key ^ seed)} (hash.hpp:27)
+//   scatter_to_parts  engine.hpp:412-474        part = mul_hi(P, h); part-major order;
+//                                               kOversubscribed if a part has > S keys
+//   per-part sort     engine.hpp:505-518        std::sort of each part's slice, then
+//                                               kDuplicateHashes on equal neighbours
+// part = hi(P * h) is monotone in h, so sorting all hashes by h gives exactly the
+// part-major arrangement with every part sorted. This file produces that array and the
+// part offsets on the device: a hash kernel, a device radix sort of the u64 hashes
+// (CUB, from the CUDA toolkit: construction is off the hot path), and a kernel that writes
+// the part boundaries and checks both failure conditions.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstdint>
+
+#include "ph_device.cuh"
+#include "ph_kernels.h"
+
+namespace phg {
+namespace {
+
+__global__ void __launch_bounds__(256) k_hash_u64(const uint64_t* __restrict__ keys, uint64_t n,
+                                                  uint64_t seed, uint64_t* __restrict__ h) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        h[i] = kC * (keys[i] ^ seed);  // hash_int, hash.hpp:27
+}
+
+__device__ __forceinline__ uint64_t part_of(uint64_t P, uint64_t h) { return __umul64hi(P, h); }
+
+// offsets[p] = first index of part p in the sorted hashes (offsets[P] = n): index i writes
+// the offsets of the parts in (part(i-1), part(i)], so every offset is written once.
+// Also flags equal neighbours (engine.hpp:507-513).
+__global__ void __launch_bounds__(256) k_part_bounds(const uint64_t* __restrict__ h, uint64_t n,
+                                                     uint64_t P, uint64_t* __restrict__ offsets,
+                                                     int* __restrict__ status) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t pi = i < n ? part_of(P, h[i]) : P;
+        const uint64_t pprev = i > 0 ? part_of(P, h[i - 1]) + 1 : 0;
+        for (uint64_t p = pprev; p <= pi && p <= P; p++) offsets[p] = i;
+        if (i > 0 && i < n && h[i] == h[i - 1]) atomicOr(status, 2);
+    }
+}
+
+// kOversubscribed (engine.hpp:437-443): a part holds more than S keys.
+__global__ void __launch_bounds__(256) k_part_sizes(const uint64_t* __restrict__ offsets, uint64_t P,
+                                                    uint64_t S, int* __restrict__ status) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < P;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        if (offsets[p + 1] - offsets[p] > S) atomicOr(status, 1);
+}
+
+}  // namespace
+
+// Scratch comes from a per-device pool that keeps its memory between calls (the sort
+// needs ~n*8 bytes of it; remapping that on every call would cost more than the sort).
+static cudaError_t scratch_pool(cudaMemPool_t* pool) {
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess || dev < 0 || dev >= 64) return e != cudaSuccess ? e : cudaErrorInvalidDevice;
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if ((e = cudaMemPoolCreate(&pools[dev], &props)) != cudaSuccess) return e;
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    *pool = pools[dev];
+    return cudaSuccess;
+}
+
+cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint64_t S,
+                              uint64_t seed, uint64_t* hashes, uint64_t* offsets, int* status,
+                              cudaStream_t s, int sms) {
+    *status = 0;
+    int* d_status = nullptr;
+    uint64_t* tmp = nullptr;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    cudaMemPool_t pool = nullptr;
+    cudaError_t e = scratch_pool(&pool);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&d_status, sizeof(int), pool, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_status, 0, sizeof(int), s);
+    if (e == cudaSuccess && n) e = cudaMallocFromPoolAsync(&tmp, n * 8, pool, s);
+    const int grid = sms * 8;
+    if (e == cudaSuccess && n) {
+        k_hash_u64<<<grid, 256, 0, s>>>(keys, n, seed, tmp);
+        note_launch();
+        e = cudaGetLastError();
+    }
+    // sort tmp -> hashes (all 64 bits: the part is the high-order function of h)
+    if (e == cudaSuccess && n)
+        e = cub::DeviceRadixSort::SortKeys(nullptr, cub_bytes, tmp, hashes, n, 0, 64, s);
+    if (e == cudaSuccess && n) e = cudaMallocFromPoolAsync(&cub_tmp, cub_bytes, pool, s);
+    if (e == cudaSuccess && n) {
+        e = cub::DeviceRadixSort::SortKeys(cub_tmp, cub_bytes, tmp, hashes, n, 0, 64, s);
+        note_launch();
+    }
+    if (e == cudaSuccess) {
+        k_part_bounds<<<grid, 256, 0, s>>>(hashes, n, P, offsets, d_status);
+        note_launch();
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        k_part_sizes<<<grid, 256, 0, s>>>(offsets, P, S, d_status);
+        note_launch();
+        e = cudaGetLastError();
+    }
+    int h_status = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (cub_tmp) cudaFreeAsync(cub_tmp, s);
+    if (tmp) cudaFreeAsync(tmp, s);
+    if (d_status) cudaFreeAsync(d_status, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    // as run_attempt (construction.cpp:42-52): an oversubscribed part fails the scatter
+    // before any part is sorted
+    *status = (h_status & 1) ? 1 : (h_status & 2) ? 2 : 0;
+    return e;
+}
+
+}  // namespace phg

@@ -91,6 +91,11 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
 void set_pass_timing(bool on);
 int pass_times(double* ms_sums, int* calls);
 
+// Construction assist (ph_build.cu): hash + sort + part offsets, synchronous on s.
+cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint64_t S,
+                              uint64_t seed, uint64_t* hashes, uint64_t* offsets, int* status,
+                              cudaStream_t s, int sms);
+
 cudaError_t launch_relayout(const uint8_t* src, uint8_t* dst, uint64_t P, uint64_t B, uint64_t H,
                             cudaStream_t s);
 cudaError_t launch_verify(const void* out, int out_width, uint64_t count, uint64_t n,

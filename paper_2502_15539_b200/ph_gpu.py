@@ -118,6 +118,27 @@ _L.ph_gpu_set_pass_timing.argtypes = [C.c_int]
 _L.ph_gpu_pass_times.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int)]
 
 
+_L.ph_gpu_build_prepare_u64.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint64,
+                                        C.c_uint64, C.c_int, C.c_void_p, C.c_void_p,
+                                        C.POINTER(C.c_int)]
+
+
+def build_prepare_u64(keys, parts: int, slots_per_part: int, seed: int, device: int = 0):
+    """Construction assist (ph_gpu_build_prepare_u64): the hashes of the CUDA u64 tensor
+    `keys` in part-major, per-part-sorted order, the part offsets, and the status
+    (0 ok, 1 oversubscribed part, 2 duplicate hashes)."""
+    import torch
+    n = keys.numel()
+    hashes = torch.empty(n, dtype=torch.int64, device=keys.device)
+    offsets = torch.empty(parts + 1, dtype=torch.int64, device=keys.device)
+    st = C.c_int(0)
+    _check(_L.ph_gpu_build_prepare_u64(C.c_void_p(keys.data_ptr() if n else 0), n, parts,
+                                       slots_per_part, seed, device,
+                                       C.c_void_p(hashes.data_ptr() if n else 0),
+                                       C.c_void_p(offsets.data_ptr()), C.byref(st)))
+    return hashes, offsets, st.value
+
+
 def set_pass_timing(on: bool):
     """Record CUDA events around the partitioned path's passes (profiling aid)."""
     _check(_L.ph_gpu_set_pass_timing(1 if on else 0))

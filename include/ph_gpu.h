@@ -129,6 +129,14 @@ int ph_gpu_build_prepare_u64(const uint64_t* d_keys, size_t n, uint64_t parts,
                              uint64_t slots_per_part, uint64_t seed, int device,
                              uint64_t* d_hashes, uint64_t* d_offsets, int* status);
 
+/* Build statistics (stats.cpp:59-61; recorded by group_buckets, engine.hpp:304-322) on the
+ * index's device, synchronous: hist[s] = number of the P*B buckets holding s of the u64 keys
+ * d_keys[0..n) (the key set the index was built from gives the reference's
+ * bucket_size_counts). *len = largest size + 1; min(cap, *len) entries are written.
+ * PH_E_UNSUPPORTED if a bucket holds more than 2^24 keys. */
+int ph_gpu_bucket_sizes(const ph_gpu_index* index, const uint64_t* d_keys, size_t n,
+                        uint64_t* hist, size_t cap, size_t* len);
+
 /* ---- verification ---- */
 /* verify_bijection (proj/tools/ptrhash.cpp:186-210) on `device`, synchronous: counts the
  * outputs >= n and the repeated outputs among d_out[0..count) (u32 or u64). */

@@ -90,6 +90,9 @@ class Ref:
         L.ref_clef_get.restype = C.c_uint64
         L.ref_build_prepare_u64.argtypes = [u64p, C.c_size_t, C.c_uint64, C.c_uint64,
                                             C.c_uint64, C.c_uint, u64p, u64p]
+        L.ref_build_u64_stats.argtypes = [u64p, C.c_size_t, C.POINTER(RefParams), C.c_uint,
+                                          C.POINTER(u8p), C.POINTER(C.c_size_t), u64p,
+                                          C.c_size_t, C.POINTER(C.c_size_t)]
         L.ref_hw_threads.restype = C.c_uint
 
     # ---- params / shape ----
@@ -137,6 +140,16 @@ class Ref:
         rc = self.L.ref_build_u64(_ptr(keys), keys.size, C.byref(params), threads,
                                   C.byref(out), C.byref(ln))
         return self._take(rc, out, ln)
+
+    def build_u64_stats(self, keys: np.ndarray, params: RefParams, threads: int = 0):
+        """build() with BuildStats: (PTRH bytes, bucket_size_counts) (stats.cpp:59-61)."""
+        k = np.ascontiguousarray(keys, dtype=np.uint64)
+        out, ln = u8p(), C.c_size_t()
+        sizes = np.zeros(4096, dtype=np.uint64)
+        slen = C.c_size_t()
+        rc = self.L.ref_build_u64_stats(_ptr(k), k.size, C.byref(params), threads, C.byref(out),
+                                        C.byref(ln), _ptr(sizes), sizes.size, C.byref(slen))
+        return self._take(rc, out, ln), sizes[: min(slen.value, sizes.size)].copy()
 
     def build_u64_shape(self, keys, params, P, S, B, threads=0) -> bytes:
         keys = np.ascontiguousarray(keys, dtype=np.uint64)

@@ -184,6 +184,20 @@ int ref_build_u64_shape(const uint64_t* keys, size_t n, const RefParams* p, uint
     });
 }
 
+// build() with BuildStats: also returns bucket_size_counts (stats.cpp:59-61).
+int ref_build_u64_stats(const uint64_t* keys, size_t n, const RefParams* p, unsigned threads,
+                        uint8_t** out, size_t* out_len, uint64_t* sizes, size_t cap,
+                        size_t* sizes_len) {
+    return guarded([&] {
+        BuildStats st;
+        PtrHashIndex idx = build(std::span<const uint64_t>(keys, n), to_params(p), threads, &st);
+        *sizes_len = st.bucket_size_counts.size();
+        for (size_t i = 0; i < cap && i < st.bucket_size_counts.size(); i++)
+            sizes[i] = st.bucket_size_counts[i];
+        return emit(idx, out, out_len);
+    });
+}
+
 // build(span<std::string>) — the reference's string builder (memory heavy).
 int ref_build_bytes(const uint8_t* data, const uint64_t* offsets, size_t n, const RefParams* p,
                     unsigned threads, uint8_t** out, size_t* out_len) {

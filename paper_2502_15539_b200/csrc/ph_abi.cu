@@ -1087,4 +1087,19 @@ int ph_gpu_build_prepare_u64(const uint64_t* d_keys, size_t n, uint64_t parts,
     return e == cudaSuccess ? PH_OK : cuda_fail(e, "build_prepare_u64");
 }
 
+int ph_gpu_bucket_sizes(const ph_gpu_index* index, const uint64_t* d_keys, size_t n,
+                        uint64_t* hist, size_t cap, size_t* len) {
+    if (!index || (!d_keys && n) || !len || (!hist && cap)) return fail(PH_E_INVALID, "null argument");
+    if (index->info.key_kind != 0) return fail(PH_E_KEYKIND, "index was built over byte-string keys");
+    DeviceGuard g(index->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    uint64_t l = 0;
+    const cudaError_t e = phg::bucket_size_hist(index->dev, index->info.bucket_fn, d_keys, n, hist,
+                                                cap, &l, nullptr, index->sms);
+    if (e == cudaErrorNotSupported) return fail(PH_E_UNSUPPORTED, "a bucket holds more than 2^24 keys");
+    if (e != cudaSuccess) return cuda_fail(e, "bucket_sizes");
+    *len = l;
+    return PH_OK;
+}
+
 }  // extern "C"

@@ -17,6 +17,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ph_device.cuh"
@@ -125,6 +126,105 @@ cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint
     // as run_attempt (construction.cpp:42-52): an oversubscribed part fails the scatter
     // before any part is sorted
     *status = (h_status & 1) ? 1 : (h_status & 2) ? 2 : 0;
+    return e;
+}
+
+// ---------------------------------------------------------------------------------------
+// Bucket-size statistics (stats.cpp:59-61, recorded by group_buckets, engine.hpp:304-322):
+// hist[s] = number of the P*B buckets that hold s of the keys.
+// ---------------------------------------------------------------------------------------
+namespace {
+
+template <int G>
+__global__ void __launch_bounds__(256) k_bucket_count(const DevIndex ix,
+                                                      const uint64_t* __restrict__ keys,
+                                                      uint64_t n, uint32_t* __restrict__ cnt) {
+    const uint32_t P32 = (uint32_t)ix.P, B32 = (uint32_t)ix.B;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = kC * (keys[i] ^ ix.seed);  // hash_int, hash.hpp:27
+        uint64_t x, unused;
+        const uint32_t part = (uint32_t)mul32x64(P32, h, x);  // part_and_bucket, bucket_fn.hpp:66-72
+        const uint32_t bucket = (uint32_t)mul32x64(B32, gamma<G>(x, ix.opt_table), unused);
+        atomicAdd(cnt + (uint64_t)part * B32 + bucket, 1u);
+    }
+}
+
+constexpr int kHistBins = 64;  // per-block shared bins for sizes < 63
+constexpr uint32_t kMaxHistSize = 1u << 24;
+
+__global__ void __launch_bounds__(256) k_bucket_hist(const uint32_t* __restrict__ cnt,
+                                                     uint64_t nb, unsigned long long* __restrict__ hist,
+                                                     uint32_t* __restrict__ max_size) {
+    __shared__ unsigned long long sh[kHistBins];
+    if (threadIdx.x < kHistBins) sh[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t mx = 0;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = cnt[b];
+        mx = max(mx, c);
+        if (c < kHistBins - 1) atomicAdd(&sh[c], 1ull);
+        else atomicAdd(hist + min(c, kMaxHistSize), 1ull);  // rare large buckets
+    }
+    __syncthreads();
+    if (threadIdx.x < kHistBins - 1 && sh[threadIdx.x]) atomicAdd(hist + threadIdx.x, sh[threadIdx.x]);
+    atomicMax(max_size, mx);
+}
+
+template <int G>
+cudaError_t bucket_count(const DevIndex& ix, const uint64_t* keys, uint64_t n, uint32_t* cnt,
+                         cudaStream_t s, int sms) {
+    k_bucket_count<G><<<sms * 8, 256, 0, s>>>(ix, keys, n, cnt);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t bucket_size_hist(const DevIndex& ix, int gamma_kind, const uint64_t* keys, uint64_t n,
+                             uint64_t* hist_out, uint64_t cap, uint64_t* len_out, cudaStream_t s,
+                             int sms) {
+    const uint64_t nb = ix.P * ix.B;
+    cudaMemPool_t pool = nullptr;
+    cudaError_t e = scratch_pool(&pool);
+    uint32_t* cnt = nullptr;
+    unsigned long long* hist = nullptr;  // counts for sizes 0..n (a bucket holds at most n keys)
+    uint32_t* mx = nullptr;
+    // sizes up to 2^24 (a bucket holds at most n keys); larger ones are reported as an error
+    const uint64_t hbins = std::max<uint64_t>(std::min<uint64_t>(n, kMaxHistSize) + 1, kHistBins);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&cnt, nb * 4, pool, s);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&hist, hbins * 8 + 8, pool, s);
+    if (e == cudaSuccess) {
+        mx = reinterpret_cast<uint32_t*>(hist + hbins);
+        e = cudaMemsetAsync(cnt, 0, nb * 4, s);
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, hbins * 8 + 8, s);
+    if (e == cudaSuccess && n) {
+        switch (gamma_kind) {
+            case 0: e = bucket_count<0>(ix, keys, n, cnt, s, sms); break;
+            case 1: e = bucket_count<1>(ix, keys, n, cnt, s, sms); break;
+            case 2: e = bucket_count<2>(ix, keys, n, cnt, s, sms); break;
+            case 3: e = bucket_count<3>(ix, keys, n, cnt, s, sms); break;
+            case 4: e = bucket_count<4>(ix, keys, n, cnt, s, sms); break;
+            default: e = cudaErrorInvalidValue;
+        }
+    }
+    if (e == cudaSuccess) {
+        k_bucket_hist<<<sms * 8, 256, 0, s>>>(cnt, nb, hist, mx);
+        note_launch();
+        e = cudaGetLastError();
+    }
+    uint32_t h_mx = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_mx, mx, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && h_mx > kMaxHistSize) e = cudaErrorNotSupported;
+    if (e == cudaSuccess) {
+        *len_out = (uint64_t)h_mx + 1;
+        e = cudaMemcpy(hist_out, hist, std::min<uint64_t>(cap, *len_out) * 8, cudaMemcpyDeviceToHost);
+    }
+    if (hist) cudaFreeAsync(hist, s);
+    if (cnt) cudaFreeAsync(cnt, s);
     return e;
 }
 

@@ -96,6 +96,11 @@ cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint
                               uint64_t seed, uint64_t* hashes, uint64_t* offsets, int* status,
                               cudaStream_t s, int sms);
 
+// Bucket-size histogram of a key set (stats.cpp:59-61): hist_out[s] for s < min(cap, *len).
+cudaError_t bucket_size_hist(const DevIndex& ix, int gamma_kind, const uint64_t* keys, uint64_t n,
+                             uint64_t* hist_out, uint64_t cap, uint64_t* len_out, cudaStream_t s,
+                             int sms);
+
 cudaError_t launch_relayout(const uint8_t* src, uint8_t* dst, uint64_t P, uint64_t B, uint64_t H,
                             cudaStream_t s);
 cudaError_t launch_verify(const void* out, int out_width, uint64_t count, uint64_t n,

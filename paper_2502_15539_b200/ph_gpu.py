@@ -118,6 +118,8 @@ _L.ph_gpu_set_pass_timing.argtypes = [C.c_int]
 _L.ph_gpu_pass_times.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int)]
 
 
+_L.ph_gpu_bucket_sizes.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
+                                   C.POINTER(C.c_size_t)]
 _L.ph_gpu_build_prepare_u64.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint64,
                                         C.c_uint64, C.c_int, C.c_void_p, C.c_void_p,
                                         C.POINTER(C.c_int)]
@@ -194,6 +196,17 @@ class PtrHashIndex:
                                           out.element_size(), int(self.info.n if n is None else n),
                                           int(self.info.device), C.byref(oob), C.byref(dup)))
         return int(oob.value), int(dup.value)
+
+    def bucket_sizes(self, keys):
+        """ph_gpu_bucket_sizes: hist[s] = number of buckets holding s of the keys (CUDA u64
+        tensor); for the build's key set this is the reference's bucket_size_counts."""
+        import numpy as np
+        cap = 4096
+        hist = np.zeros(cap, dtype=np.uint64)
+        ln = C.c_size_t(0)
+        _check(_L.ph_gpu_bucket_sizes(self._h, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                      C.c_void_p(hist.ctypes.data), cap, C.byref(ln)))
+        return hist[: min(ln.value, cap)].copy()
 
     def set_l2_policy(self, hot_bytes: int, flags: int = 0):
         """Pilot layout / L2 policy (ph_gpu_index_set_l2_policy); results are unaffected."""

@@ -45,3 +45,22 @@ def test_gpu_build_prepare_matches_reference(ref):
         if st != 1:
             assert np.array_equal(h.cpu().numpy().view(np.uint64), h_r), name
             assert np.array_equal(off.cpu().numpy().view(np.uint64), off_r), name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset,fn", [("default", None), ("fast", None), ("default", "quadratic"),
+                                       ("default", "skewed"), ("default", "optimal")])
+def test_gpu_bucket_sizes_match_reference_stats(ref, preset, fn):
+    """ph_gpu_bucket_sizes over the build's key set equals the reference's
+    BuildStats::bucket_size_counts (stats.cpp:59-61) for every bucket function."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2502_15539_b200 import ph_gpu
+    keys = corpus_u64_np(0, 400_000, 82)
+    params = ref.params(preset, lambda_=(30, 10)) if fn is None else \
+        ref.params(preset, lambda_=(30, 10), bucket_fn=fn)
+    ptrh, want = ref.build_u64_stats(keys, params)
+    idx = ph_gpu.PtrHashIndex(ptrh)
+    got = idx.bucket_sizes(torch.from_numpy(keys.view(np.int64)).cuda())
+    assert np.array_equal(got, want), (preset, fn)

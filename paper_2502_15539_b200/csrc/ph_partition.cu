@@ -267,8 +267,10 @@ constexpr int kBinTmaThreads = PH_BIN_TMA_THREADS;
 constexpr size_t kBinTmaSmem = 2 * kTileKeys * 8 + kBinTmaStage * (8 + 2);
 
 // Pass A, bulk-copy variant (u64 keys, 16-B aligned key array).
-// SRC = 1: keys are the k-mers of a packed sequence (seq_words, kbits), read with ordinary
-// loads (0.25 B per key); only the run stores use the bulk-copy engine.
+// SRC = 1: keys are the k-mers of a packed sequence (seq_words, kbits): a tile's windows
+// need its kSeqWords packed words (0.25 B per key), which arrive by bulk load like u64 key
+// tiles, and each window is extracted from shared memory.
+constexpr uint32_t kSeqWords = kTileKeys / 32 + 2;  // 130: 16-B multiple for 4096-key tiles
 template <int THREADS, int SRC>
 __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
     const uint64_t* __restrict__ keys, uint64_t n, uint64_t seq_words, uint32_t kbits,
@@ -287,9 +289,16 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
     constexpr int PER = kTileKeys / THREADS;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
-    // tiles that arrive by bulk load (u64 keys only)
-    const uint64_t nfull = n / kTileKeys;
-    auto bulk = [&](uint64_t t) { return SRC == 0 && t < nfull; };
+    // tiles that arrive by bulk load: whole u64 key tiles, or (k-mers) tiles whose
+    // kSeqWords words all lie inside the sequence
+    const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+    const uint64_t nfull =
+        !aligned ? 0
+        : SRC == 0 ? n / kTileKeys
+                   : (seq_words >= kSeqWords
+                          ? min((seq_words - kSeqWords) / (kTileKeys / 32) + 1, ntiles)
+                          : 0);
+    auto bulk = [&](uint64_t t) { return t < nfull; };
     const uint64_t pol = policy_evict_first();
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -298,9 +307,11 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
     }
     if (tid < kTmaGroups) cnt[0][tid] = 0;
     __syncthreads();
-    auto issue = [&](uint64_t t, int b) {  // thread 0: bulk-load full tile t into buffer b
-        mbar_expect_tx(&bar[b], kTileKeys * 8);
-        bulk_g2s(in + b * kTileKeys, keys + t * kTileKeys, kTileKeys * 8, &bar[b], pol);
+    auto issue = [&](uint64_t t, int b) {  // thread 0: bulk-load tile t's input into buffer b
+        constexpr uint32_t bytes = SRC == 1 ? kSeqWords * 8 : kTileKeys * 8;
+        mbar_expect_tx(&bar[b], bytes);
+        bulk_g2s(in + b * kTileKeys, keys + t * (SRC == 1 ? kTileKeys / 32 : kTileKeys), bytes,
+                 &bar[b], pol);
     };
     if (tid == 0) {
         if (bulk(blockIdx.x)) issue(blockIdx.x, 0);
@@ -312,7 +323,31 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
         const uint64_t t0 = t * kTileKeys;
         const uint32_t valid = (uint32_t)(n - t0 < kTileKeys ? n - t0 : kTileKeys);
         uint64_t k[PER];
-        if (bulk(t)) {
+        if (SRC == 1) {
+            // k-mers: the tile's packed words (each serves 32 consecutive windows) sit in
+            // shared memory -- bulk-loaded ahead, or (last tiles) loaded here -- and every
+            // window is extracted from there (kmer_at's layout)
+            const uint64_t w0 = t0 >> 5;
+            uint64_t* wv = in + b * kTileKeys;
+            if (bulk(t)) {
+                mbar_wait(&bar[b], (it >> 1) & 1);
+            } else {
+                const uint64_t left = seq_words - w0;
+                const uint32_t nw = (uint32_t)(left < kSeqWords ? left : kSeqWords);
+                for (uint32_t q = tid; q < nw; q += THREADS) wv[q] = __ldg(keys + w0 + q);
+                __syncthreads();
+            }
+#pragma unroll
+            for (int j = 0; j < PER; j++) {
+                const uint32_t e = (uint32_t)j * THREADS + tid;
+                const uint64_t i = t0 + e;
+                const uint32_t a = (uint32_t)((i >> 5) - w0), o = (uint32_t)(i & 31) * 2;
+                const uint64_t wa = wv[a];
+                const uint64_t wb = (o && w0 + a + 1 < seq_words) ? wv[a + 1] : 0;
+                const uint64_t top = o ? (wa << o) | (wb >> (64 - o)) : wa;
+                k[j] = e < valid ? (kbits == 64 ? top : top >> (64 - kbits)) : 0;
+            }
+        } else if (bulk(t)) {
             mbar_wait(&bar[b], (it >> 1) & 1);
 #pragma unroll
             for (int j = 0; j < PER; j++) k[j] = in[b * kTileKeys + j * THREADS + tid];
@@ -320,10 +355,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
 #pragma unroll
             for (int j = 0; j < PER; j++) {
                 const uint32_t e = (uint32_t)j * THREADS + tid;
-                if (SRC == 1)
-                    k[j] = e < valid ? part_kmer(keys, seq_words, t0 + e, kbits) : 0;
-                else
-                    k[j] = e < valid ? __ldcs(keys + t0 + e) : 0;
+                k[j] = e < valid ? __ldcs(keys + t0 + e) : 0;
             }
         }
         uint32_t* c_ = cnt[b];

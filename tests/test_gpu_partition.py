@@ -183,3 +183,25 @@ def test_pass_timing_records_three_passes(ph, ref):
         assert ph.pass_times()[1] == 1
     finally:
         ph.set_pass_timing(False)
+
+
+@pytest.mark.parametrize("n_bases,k,woff", [(100, 31, 0), (4096 + 30, 31, 0), (130 * 32 + 31, 31, 0),
+                                            (300_017, 31, 1), (300_017, 16, 0), (250_000, 32, 1),
+                                            (200_003, 9, 0)])
+def test_partitioned_kmers_edges(ph, ref, port, n_bases, k, woff):
+    """Partitioned k-mer path: partial and single tiles, the last tiles whose 130 packed
+    words run past the sequence (loaded without the bulk engine), other k, and a sequence
+    that is only 8-B aligned (woff = 1: no bulk loads at all)."""
+    seq = port.gen_dna(n_bases, 46 + k)
+    kmers = port.kmers(seq, n_bases, k)
+    uniq = np.unique(kmers)
+    ptrh = ref.build_u64(uniq, ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    buf = torch.zeros(seq.size + woff, dtype=torch.int64, device="cuda")
+    buf[woff:] = torch.from_numpy(seq.view(np.int64)).cuda()
+    for minimal in (True, False):
+        want = ri.query_u64(kmers, minimal, "loop", threads=THREADS)
+        out = idx.query_kmers(buf[woff:], n_bases, k, minimal=minimal, out_width=8)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (n_bases, k, woff, minimal)

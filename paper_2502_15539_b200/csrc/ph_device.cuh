@@ -44,7 +44,7 @@ struct DevIndex {
     uint64_t window_bytes;        // persisting window over the hot region (0 = none)
     float window_hit_ratio;
     int32_t cold_evict_first;     // cold-region pilot loads: 1 = L2::evict_first, 0 = evict_last
-    int32_t pilot_evict_normal;   // 1: all pilot loads L2::evict_normal (partitioned pass B)
+    int32_t pilot_evict_normal;   // 1: pilot loads L2::evict_normal instead of evict_last (A/B knob)
     // AES string hash round keys k0/k1 (hash.cpp:116-119) as LE u32 words, host-derived
     uint32_t aes_k0[4], aes_k1[4];
 };

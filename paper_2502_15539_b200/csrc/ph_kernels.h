@@ -12,16 +12,15 @@ namespace phg {
 
 // Launch `kernel` with the index's persisting-L2 access-policy window over the hot
 // pilot region (a per-launch attribute: the caller's stream is not modified).
-// pdl: programmatic dependent launch (cudaLaunchAttributeProgrammaticStreamSerialization).
 template <class... KArgs, class... Args>
-inline cudaError_t launch_ex_pdl(const DevIndex& ix, bool pdl, void (*kernel)(KArgs...),
-                                 unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
+                             unsigned block, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[1];
     unsigned na = 0;
     if (ix.window_bytes) {
         attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -32,19 +31,9 @@ inline cudaError_t launch_ex_pdl(const DevIndex& ix, bool pdl, void (*kernel)(KA
         attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         na++;
     }
-    if (pdl) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        na++;
-    }
     cfg.attrs = na ? attr : nullptr;
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
-}
-template <class... KArgs, class... Args>
-inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
-                             unsigned block, cudaStream_t s, Args... args) {
-    return launch_ex_pdl(ix, false, kernel, grid, block, s, args...);
 }
 
 // Scratch for the deferred remap (k_remap_patch); idx == nullptr selects the inline
@@ -71,12 +60,6 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                                uint64_t n_bases, int k, void* out, int out_width, int minimal,
                                cudaStream_t s, int sms,
                                const RemapList& rl = RemapList{nullptr, nullptr, nullptr, 0});
-
-// Same as launch_query_u64 with the L2-resident tuning forced (partitioned pass B).
-cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2,
-                                   const uint64_t* keys, void* out, int out_width, uint64_t n,
-                                   int minimal, cudaStream_t s, int sms, const RemapList& rl,
-                                   bool l2_tuning);
 
 // Partitioned path (ph_partition.cu). src_kind 0: keys = u64 keys; 1: keys = packed
 // sequence (seq_words, kbits), n = number of windows. scratch >= partition_scratch_bytes.

@@ -246,7 +246,6 @@ struct KeySrc {
     int kind;  // 0 = u64 array, 1 = k-mers
     uint64_t seq_words;
     uint32_t kbits;
-    int tuning;  // 0 = by pilot size, 1 = L2-resident tuning
 };
 
 // Two tunings of the same kernel, chosen per index by the pilot array's size
@@ -290,7 +289,7 @@ static cudaError_t launch_u64_t(const DevIndex& ix, const KeySrc& src, void* out
     const bool hotf = ix.hot_b < ix.B;
     {
         const bool dram = hotf || g_regime == 2 ||
-                          (g_regime == 0 && src.tuning == 0 && ix.P * ix.B > kDramRegimeBytes);
+                          (g_regime == 0 && ix.P * ix.B > kDramRegimeBytes);
         if (dram && hotf)
             return launch_u64_k<G, POW2, OutT, SRC, 8, 1, false, true>(ix, src, out, n, minimal, s,
                                                                        sms, rl);
@@ -337,7 +336,7 @@ static cudaError_t launch_src(const DevIndex& ix, int gamma_kind, bool pow2, con
 cudaError_t launch_query_u64(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* keys,
                              void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                              int sms, const RemapList& rl) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, 0}, out, out_width, n, minimal, s,
+    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0}, out, out_width, n, minimal, s,
                       sms, rl);
 }
 
@@ -346,16 +345,8 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                                cudaStream_t s, int sms, const RemapList& rl) {
     if (n_bases < (uint64_t)k) return cudaSuccess;
     const uint64_t n = n_bases - (uint64_t)k + 1;
-    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k), 0},
+    return launch_src(ix, gamma_kind, pow2, KeySrc{seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k)},
                       out, out_width, n, minimal, s, sms, rl);
-}
-
-cudaError_t launch_query_u64_tuned(const DevIndex& ix, int gamma_kind, bool pow2,
-                                   const uint64_t* keys, void* out, int out_width, uint64_t n,
-                                   int minimal, cudaStream_t s, int sms, const RemapList& rl,
-                                   bool l2_tuning) {
-    return launch_src(ix, gamma_kind, pow2, KeySrc{keys, 0, 0, 0, l2_tuning ? 1 : 0}, out,
-                      out_width, n, minimal, s, sms, rl);
 }
 
 // ---------------------------------------------------------------------------

@@ -155,7 +155,7 @@ int ph_gpu_set_defer_min(uint64_t min_keys);
  * restored to input order. Needs the file-order pilot layout without a persisting window
  * (the default for pilot arrays > 64 MiB) and ~30 B/key of stream-ordered scratch from the
  * index's pool (falls back to the direct kernel if it cannot be had).
- * 0 = automatic (DRAM-sized pilot arrays, batches >= pilot_bytes/2 keys), 1 = never,
+ * 0 = automatic (DRAM-sized pilot arrays, batches >= pilot_bytes/32 keys), 1 = never,
  * 2 = whenever the layout allows. Results are identical. */
 int ph_gpu_set_partition(int mode);
 /* Profiling aid (one host thread): when on, partitioned-path calls record CUDA events around

@@ -323,13 +323,13 @@ struct DeferScratch {
 };
 
 // Partitioned path (ph_partition.cu): for DRAM-sized pilot arrays and large
-// device-resident batches, keys are binned into G hash groups whose pilot slices (~12 MiB
+// device-resident batches, keys are binned into G hash groups whose pilot slices (32 MiB
 // each) stay L2-resident while pass B answers them group after group, then un-permuted.
-// It needs the file-order pilot layout without a persisting set-aside
-// (ph_gpu_index_set_l2_policy(index, 0, 2)); "auto" then uses it for batches of at least
-// pilot_bytes / 2 keys (u64 keys and k-mer windows). Measured at config 3: 11.5 ms against
-// 15.3 ms for the direct kernel on the default hot-first layout; config 5 (k-mers): 13.3 ms
-// against 13.9 ms (profiles/r01_bench_config{3,5}.json, r01_synth_*).
+// It needs the file-order pilot layout without a persisting set-aside (the default for
+// DRAM-sized arrays); "auto" uses it for batches of at least pilot_bytes / 32 keys (u64 keys
+// and k-mer windows): the break-even against the direct kernel is ~1e7 keys at config 3
+// (profiles/r01_partition_batch_sizes.txt). At 1e9 keys: 10.2 ms against 15.3 ms for the
+// direct kernel on the hot-first layout; config 5 (k-mers) 10.8 ms against 13.9 ms.
 std::atomic<int> g_partition{0};  // 0 auto, 1 off, 2 force when the layout allows
 
 uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n, int out_width) {
@@ -339,7 +339,7 @@ uint32_t partition_groups(const ph_gpu_index* ix, uint64_t n, int out_width) {
     // pass B stores non-minimal slots (minimal: remapped) in the output width
     if (out_width == PH_OUT_U32 && ix->info.parts * ix->info.slots_per_part > (uint64_t{1} << 32))
         return 0;
-    if (mode == 0 && (pb <= (uint64_t{64} << 20) || n < pb / 2 || ix->dev.window_bytes))
+    if (mode == 0 && (pb <= (uint64_t{64} << 20) || n < pb / 32 || ix->dev.window_bytes))
         return 0;
     // pilot bytes per group (L2-resident with pass B's evict_last loads). Fewer, larger
     // groups mean longer runs, i.e. fewer bulk copies and atomics in passes A and C; the

@@ -205,3 +205,43 @@ def test_partitioned_kmers_edges(ph, ref, port, n_bases, k, woff):
         out = idx.query_kmers(buf[woff:], n_bases, k, minimal=minimal, out_width=8)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (n_bases, k, woff, minimal)
+
+
+def test_partitioned_concurrent_streams(ph, ref):
+    """Several host threads query one index through the partitioned path on their own
+    streams at once (per-call scratch from the index's stream-ordered pool): every output
+    equals the reference's."""
+    import threading
+    from oracle.bindings import corpus_u64_np
+    n = 250_000
+    keys = corpus_u64_np(0, n, 69)
+    ptrh = ref.build_u64(keys, ref.params("default", lambda_=(30, 10)))
+    ri = ref.load(ptrh)
+    idx = ph.PtrHashIndex(ptrh)
+    qs = [corpus_u64_np(0, 1_500_000 + 4097 * t, 70 + t) for t in range(4)]
+    for q in qs:
+        q[:n] = keys
+    wants = [ri.query_u64(q, True, "loop", threads=THREADS) for q in qs]
+    outs = [None] * len(qs)
+    errs = []
+
+    def work(t):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                d = torch.from_numpy(qs[t].view(np.int64)).cuda()
+                for _ in range(3):
+                    o = idx.query(d, minimal=True, out_width=4, stream=s.cuda_stream)
+                s.synchronize()
+                outs[t] = o.cpu().numpy().view(np.uint32).astype(np.uint64)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(len(qs))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    for t in range(len(qs)):
+        assert np.array_equal(outs[t], wants[t]), t

@@ -539,9 +539,9 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
 
 // Pass B: the query arithmetic over the group regions (region r < G: group r, r == G: the
 // spill), non-minimal slots into slots[] at the same entry index (remap_slot happens in
-// pass C). CTAs claim 2048-entry chunks in order from a global counter, so the chunks in
-// flight always form one contiguous window (one or two regions): the current pilot slice
-// stays L2-resident. Dynamic claiming also keeps the pass balanced when it shares the SMs
+// pass C). CTAs claim batches of 2048-entry chunks in order from a global counter, so the
+// chunks in flight always form one contiguous window (one or two regions): the current
+// pilot slice stays L2-resident. Dynamic claiming also keeps the pass balanced when it shares the SMs
 // with another chunk's pass A or C.
 constexpr int kQThreads = 256;
 #ifndef PH_QB_PER
@@ -551,6 +551,9 @@ constexpr int kQPer = PH_QB_PER;                      // keys per thread (pairs)
 constexpr uint32_t kQChunk = kQThreads * kQPer;       // 2048 entries per chunk
 #ifndef PH_QB_MINB
 #define PH_QB_MINB 4
+#endif
+#ifndef PH_QB_CLAIM
+#define PH_QB_CLAIM 8  // chunks per claim, one CTA barrier per claim (1, 2, 4, 8, 16, 32 swept: 8-16 best, ~1 %)
 #endif
 
 template <int G, bool POW2, class OutT>
@@ -579,9 +582,10 @@ __global__ void __launch_bounds__(kQThreads, PH_QB_MINB) k_query_regions(
     const uint32_t P32 = (uint32_t)ix.P, B32 = (uint32_t)ix.B, S32 = (uint32_t)ix.S;
     uint32_t r = 0;
     for (int k = 0;; k ^= 1) {
-        const uint64_t c = claim[k];
-        if (c >= nchunks) break;
+        const uint64_t c0 = claim[k] * PH_QB_CLAIM;  // a batch of PH_QB_CLAIM chunks
+        if (c0 >= nchunks) break;
         if (tid == 0) claim[k ^ 1] = atomicAdd(ctrl + kCtrlWork, 1ull);  // next, in flight
+      for (uint64_t c = c0; c < c0 + PH_QB_CLAIM && c < nchunks; c++) {
         while (c >= cstart[r + 1]) r++;
         const uint64_t e0 = (uint64_t)r * cap + (c - cstart[r]) * kQChunk;
         const uint64_t end = rend[r];  // region lengths are multiples of 8 entries
@@ -629,6 +633,7 @@ __global__ void __launch_bounds__(kQThreads, PH_QB_MINB) k_query_regions(
                                  : "memory");
             }
         }
+      }
         __syncthreads();  // claim[k ^ 1] visible; claim[k] free for reuse
     }
 }

@@ -64,3 +64,19 @@ def test_gpu_bucket_sizes_match_reference_stats(ref, preset, fn):
     idx = ph_gpu.PtrHashIndex(ptrh)
     got = idx.bucket_sizes(torch.from_numpy(keys.view(np.int64)).cuda())
     assert np.array_equal(got, want), (preset, fn)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [0, 1, 2, 4097])
+def test_gpu_build_prepare_tiny(n):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2502_15539_b200 import ph_gpu
+    keys = corpus_u64_np(0, n, 83)
+    P, S, seed = 7, 1000, 12345
+    h_n, off_n, st_n = build_prepare_u64_np(keys, P, S, seed)
+    h, off, st = ph_gpu.build_prepare_u64(torch.from_numpy(keys.view(np.int64)).cuda(), P, S, seed)
+    assert st == st_n
+    assert np.array_equal(h.cpu().numpy().view(np.uint64), h_n)
+    assert np.array_equal(off.cpu().numpy().view(np.uint64), off_n)

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 
 #include "ph_device.cuh"
 #include "ph_kernels.h"
@@ -64,9 +65,11 @@ __global__ void __launch_bounds__(256) k_part_sizes(const uint64_t* __restrict__
 // needs ~n*8 bytes of it; remapping that on every call would cost more than the sort).
 static cudaError_t scratch_pool(cudaMemPool_t* pool) {
     static cudaMemPool_t pools[64] = {};
+    static std::mutex mu;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess || dev < 0 || dev >= 64) return e != cudaSuccess ? e : cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(mu);
     if (!pools[dev]) {
         cudaMemPoolProps props = {};
         props.allocType = cudaMemAllocationTypePinned;

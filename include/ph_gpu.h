@@ -69,6 +69,10 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
  * ph_gpu_index_create. */
 int ph_gpu_index_load(const char* path, int device, ph_gpu_index** out);
 int ph_gpu_index_destroy(ph_gpu_index* index);
+/* Returns the index's cached per-call scratch (the partitioned path keeps ~29 B/key of its
+ * largest batch in the index's memory pool between calls) to the device. Memory still in use
+ * by queries in flight is kept; later queries allocate again. */
+int ph_gpu_index_trim(const ph_gpu_index* index);
 int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out);
 const char* ph_gpu_last_error(void);
 

@@ -564,6 +564,15 @@ int ph_gpu_index_destroy(ph_gpu_index* index) {
     return PH_OK;
 }
 
+int ph_gpu_index_trim(const ph_gpu_index* index) {
+    if (!index) return fail(PH_E_INVALID, "null index");
+    if (!index->pool) return PH_OK;
+    DeviceGuard g(index->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    const cudaError_t e = cudaMemPoolTrimTo(index->pool, 0);  // only memory not in use
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "cudaMemPoolTrimTo");
+}
+
 int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flags) {
     if (!index) return fail(PH_E_INVALID, "null index");
     DeviceGuard g(index->device);

@@ -118,6 +118,7 @@ _L.ph_gpu_set_pass_timing.argtypes = [C.c_int]
 _L.ph_gpu_pass_times.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int)]
 
 
+_L.ph_gpu_index_trim.argtypes = [C.c_void_p]
 _L.ph_gpu_bucket_sizes.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
                                    C.POINTER(C.c_size_t)]
 _L.ph_gpu_build_prepare_u64.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint64,
@@ -207,6 +208,10 @@ class PtrHashIndex:
         _check(_L.ph_gpu_bucket_sizes(self._h, C.c_void_p(keys.data_ptr()), keys.numel(),
                                       C.c_void_p(hist.ctypes.data), cap, C.byref(ln)))
         return hist[: min(ln.value, cap)].copy()
+
+    def trim(self):
+        """Release the index's cached per-call scratch (ph_gpu_index_trim)."""
+        _check(_L.ph_gpu_index_trim(self._h))
 
     def set_l2_policy(self, hot_bytes: int, flags: int = 0):
         """Pilot layout / L2 policy (ph_gpu_index_set_l2_policy); results are unaffected."""

@@ -164,6 +164,23 @@ def test_partitioned_many_groups(ph, ref, slice_kb, nq, monkeypatch):
         assert np.array_equal(out.cpu().numpy().view(np.uint32).astype(np.uint64), want), minimal
 
 
+def test_trim_releases_scratch_between_calls(ph, ref):
+    """ph_gpu_index_trim after a partitioned call: later calls allocate again and agree."""
+    from oracle.bindings import corpus_u64_np
+    n = 200_000
+    keys = corpus_u64_np(0, n, 71)
+    ptrh = ref.build_u64(keys, ref.params("default", lambda_=(30, 10)))
+    idx = ph.PtrHashIndex(ptrh)
+    d_q = torch.from_numpy(keys.view(np.int64)).cuda()
+    a = idx.query(d_q, minimal=True, out_width=4)
+    torch.cuda.synchronize()
+    idx.trim()
+    b = idx.query(d_q, minimal=True, out_width=4)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert np.array_equal(np.sort(b.cpu().numpy().view(np.uint32)), np.arange(n, dtype=np.uint32))
+
+
 def test_pass_timing_records_three_passes(ph, ref):
     """ph_gpu_set_pass_timing / ph_gpu_pass_times: one partitioned call records positive
     times for the bin, query and unbin passes; direct-path calls record nothing."""

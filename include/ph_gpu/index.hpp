@@ -119,6 +119,8 @@ class PtrHashIndex {
                       ph_gpu_stream_t stream = nullptr) const {
         check(ph_gpu_query_u64(h_, d_keys, n, d_out, out_width, minimal, stream));
     }
+    // returns the cached per-call scratch of large (partitioned) batches to the device
+    void trim() const { check(ph_gpu_index_trim(h_)); }
 
   private:
     uint64_t single(uint64_t key, bool minimal) const {

@@ -144,6 +144,10 @@ int main(int argc, char** argv) {
                 bool same = true;
                 for (uint64_t i = 0; i < n; i++) same &= o32[i] == static_cast<uint32_t>(want[i]);
                 CHECK(same);
+                idx.trim();  // cached scratch released; the next call allocates again
+                std::vector<uint64_t> again(n);
+                idx.index_loop(queries, again.data(), minimal);
+                CHECK(again == want);
             }
             R.unload(ref);
         }

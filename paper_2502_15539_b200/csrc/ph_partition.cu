@@ -264,7 +264,14 @@ constexpr uint32_t kBinTmaStage = kTileKeys + 8 * kTmaGroups;  // (a multiple of
 #define PH_BIN_TMA_THREADS 512
 #endif
 constexpr int kBinTmaThreads = PH_BIN_TMA_THREADS;
-constexpr size_t kBinTmaSmem = 2 * kTileKeys * 8 + kBinTmaStage * (8 + 2);
+// input buffers: a u64 key tile, or (k-mers) the tile's kSeqWords packed words
+template <int SRC>
+constexpr uint32_t bin_in_words() { return SRC == 1 ? (kTileKeys / 32 + 2 + 1) & ~1u : kTileKeys; }
+template <int SRC>
+constexpr size_t bin_tma_smem() { return 2 * bin_in_words<SRC>() * 8 + kBinTmaStage * (8 + 2); }
+#ifndef PH_BIN_KMER_CTAS
+#define PH_BIN_KMER_CTAS 3  // k-mer pass A CTAs per SM (2 KB input buffers; 3 vs 2: 3.57 vs 3.83 ms at config 5)
+#endif
 
 // Pass A, bulk-copy variant (u64 keys, 16-B aligned key array).
 // SRC = 1: keys are the k-mers of a packed sequence (seq_words, kbits): a tile's windows
@@ -272,14 +279,15 @@ constexpr size_t kBinTmaSmem = 2 * kTileKeys * 8 + kBinTmaStage * (8 + 2);
 // tiles, and each window is extracted from shared memory.
 constexpr uint32_t kSeqWords = kTileKeys / 32 + 2;  // 130: 16-B multiple for 4096-key tiles
 template <int THREADS, int SRC>
-__global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
+__global__ void __launch_bounds__(THREADS, SRC == 1 ? PH_BIN_KMER_CTAS : 2) k_bin_tma(
     const uint64_t* __restrict__ keys, uint64_t n, uint64_t seq_words, uint32_t kbits,
     uint64_t seed, uint32_t G, uint64_t cap,
     unsigned long long* __restrict__ ctrl, uint64_t* __restrict__ runoff,
     uint16_t* __restrict__ runcnt, uint64_t* __restrict__ bins, uint16_t* __restrict__ bpos) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* in = reinterpret_cast<uint64_t*>(smem);  // [2][kTileKeys]
-    uint64_t* sk = in + 2 * kTileKeys;                   // staged keys, runs 8-aligned
+    constexpr uint32_t IW = bin_in_words<SRC>();         // words per input buffer
+    uint64_t* sk = in + 2 * IW;                          // staged keys, runs 8-aligned
     uint16_t* sp = reinterpret_cast<uint16_t*>(sk + kBinTmaStage);
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t cnt[2][kTmaGroups];
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
     auto issue = [&](uint64_t t, int b) {  // thread 0: bulk-load tile t's input into buffer b
         constexpr uint32_t bytes = SRC == 1 ? kSeqWords * 8 : kTileKeys * 8;
         mbar_expect_tx(&bar[b], bytes);
-        bulk_g2s(in + b * kTileKeys, keys + t * (SRC == 1 ? kTileKeys / 32 : kTileKeys), bytes,
+        bulk_g2s(in + b * IW, keys + t * (SRC == 1 ? kTileKeys / 32 : kTileKeys), bytes,
                  &bar[b], pol);
     };
     if (tid == 0) {
@@ -328,7 +336,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
             // shared memory -- bulk-loaded ahead, or (last tiles) loaded here -- and every
             // window is extracted from there (kmer_at's layout)
             const uint64_t w0 = t0 >> 5;
-            uint64_t* wv = in + b * kTileKeys;
+            uint64_t* wv = in + b * IW;
             if (bulk(t)) {
                 mbar_wait(&bar[b], (it >> 1) & 1);
             } else {
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_bin_tma(
         } else if (bulk(t)) {
             mbar_wait(&bar[b], (it >> 1) & 1);
 #pragma unroll
-            for (int j = 0; j < PER; j++) k[j] = in[b * kTileKeys + j * THREADS + tid];
+            for (int j = 0; j < PER; j++) k[j] = in[b * IW + j * THREADS + tid];
         } else {
 #pragma unroll
             for (int j = 0; j < PER; j++) {
@@ -780,17 +788,20 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
     const bool tma = G <= (uint32_t)kTmaGroups && !std::getenv("PH_GPU_NO_TMA") &&
                      (src_kind == 1 || (reinterpret_cast<uintptr_t>(keys) & 15) == 0);
     if (tma) {
-        const uint64_t ctas = (uint64_t)sms * env_int("PH_GPU_PART_A_CTAS", 2);
+        const uint64_t ctas =
+            (uint64_t)sms * env_int("PH_GPU_PART_A_CTAS", src_kind == 1 ? PH_BIN_KMER_CTAS : 2);
         const int grid_t = (int)(want < ctas ? want : ctas);
         if (src_kind == 1) {
+            constexpr size_t sm = bin_tma_smem<1>();
             cudaFuncSetAttribute(k_bin_tma<kBinTmaThreads, 1>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinTmaSmem);
-            k_bin_tma<kBinTmaThreads, 1><<<grid_t, kBinTmaThreads, kBinTmaSmem, s>>>(
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_bin_tma<kBinTmaThreads, 1><<<grid_t, kBinTmaThreads, sm, s>>>(
                 keys, n, seq_words, kbits, ix.seed, G, L.cap, ctrl, runoff, runcnt, bins, bpos);
         } else {
+            constexpr size_t sm = bin_tma_smem<0>();
             cudaFuncSetAttribute(k_bin_tma<kBinTmaThreads, 0>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinTmaSmem);
-            k_bin_tma<kBinTmaThreads, 0><<<grid_t, kBinTmaThreads, kBinTmaSmem, s>>>(
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_bin_tma<kBinTmaThreads, 0><<<grid_t, kBinTmaThreads, sm, s>>>(
                 keys, n, 0, 0, ix.seed, G, L.cap, ctrl, runoff, runcnt, bins, bpos);
         }
     } else if (src_kind == 1) {

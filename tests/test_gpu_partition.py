@@ -262,3 +262,36 @@ def test_partitioned_concurrent_streams(ph, ref):
     assert not errs, errs
     for t in range(len(qs)):
         assert np.array_equal(outs[t], wants[t]), t
+
+
+def test_auto_partition_on_dram_sized_index(ref):
+    """Default settings end to end: an index whose pilot array exceeds 64 MiB keeps the file
+    order without a window, and a device batch above pilot_bytes/32 takes the partitioned
+    path by itself (the pass timers see it). Every key checked against the reference on a
+    sample and the minimal outputs a bijection on all of them."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle.bindings import corpus_u64_np
+    from paper_2502_15539_b200 import ph_gpu
+    n = 220_000_000
+    keys = corpus_u64_np(0, n, 84)
+    ptrh = ref.build_u64(keys, ref.params("default", lambda_=(30, 10)))
+    idx = ph_gpu.PtrHashIndex(ptrh)
+    assert idx.info.pilot_bytes > (64 << 20)
+    ph_gpu.set_partition(0)
+    d_k = torch.from_numpy(keys.view(np.int64)).cuda()
+    ph_gpu.set_pass_timing(True)
+    try:
+        out = idx.query(d_k, minimal=True, out_width=4)
+        torch.cuda.synchronize()
+        assert ph_gpu.pass_times()[1] == 1  # the partitioned path ran
+    finally:
+        ph_gpu.set_pass_timing(False)
+    oob, dups = idx.verify_bijection(out)
+    assert oob == 0 and dups == 0
+    ri = ref.load(ptrh)
+    rng = np.random.default_rng(5)
+    sample = np.sort(rng.choice(n, 2_000_000, replace=False))
+    want = ri.query_u64(keys[sample], True, "loop", threads=THREADS)
+    got = out.cpu().numpy().view(np.uint32)[sample].astype(np.uint64)
+    assert np.array_equal(got, want)

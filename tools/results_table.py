@@ -34,7 +34,7 @@ def main():
         row(5, "5 | 1e9 k-mers, fused front end, partitioned path"),
         row(4, "4 | 3e8 strings, AES, shuffled"),
         row(2, "2 | 1e8 queries, 33 MB pilots", " (L2-resident)"),
-        row(1, "1 | 1e7 u64, shuffled"),
+        row(1, "1 | 1e7 u64, shuffled", " (L2-resident)"),
     ])
     p3, p5 = d3["partition_passes"], d5["partition_passes"]
     passes = (f"Per-pass rooflines of the partitioned path (bench.py `partition_passes`, live CUDA events):\n"

@@ -13,12 +13,12 @@ namespace phg {
 // Launch `kernel` with the index's persisting-L2 access-policy window over the hot
 // pilot region (a per-launch attribute: the caller's stream is not modified).
 template <class... KArgs, class... Args>
-inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
-                             unsigned block, cudaStream_t s, Args... args) {
+inline cudaError_t launch_ex_smem(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
+                                  unsigned block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     unsigned na = 0;
@@ -34,6 +34,11 @@ inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsig
     cfg.attrs = na ? attr : nullptr;
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+template <class... KArgs, class... Args>
+inline cudaError_t launch_ex(const DevIndex& ix, void (*kernel)(KArgs...), unsigned grid,
+                             unsigned block, cudaStream_t s, Args... args) {
+    return launch_ex_smem(ix, kernel, grid, block, 0, s, args...);
 }
 
 // Scratch for the deferred remap (k_remap_patch); idx == nullptr selects the inline

@@ -40,16 +40,29 @@ __constant__ uint8_t c_sbox[256] = {
     0xe1, 0xf8, 0x98, 0x11, 0x69, 0xd9, 0x8e, 0x94, 0x9b, 0x1e, 0x87, 0xe9, 0xce, 0x55, 0x28, 0xdf,
     0x8c, 0xa1, 0x89, 0x0d, 0xbf, 0xe6, 0x42, 0x68, 0x41, 0x99, 0x2d, 0x0f, 0xb0, 0x54, 0xbb, 0x16};
 
-// One MixColumns∘SubBytes table T0[x] = (2·S[x], S[x], S[x], 3·S[x]) (rows 0..3, LE), held
-// in shared memory 32 times, interleaved so that entry x of copy `lane` sits at byte offset
-// x*128 + lane*4: every lane reads its own copy, i.e. its own bank, so the 16 lookups of an
-// AES round are conflict-free whatever the state bytes are. The rows' rotated tables are
-// T0 rotated by 8/16/24 bits, and S[x] is byte 1 of T0[x] (for AESENCLAST).
+// The MixColumns∘SubBytes tables T0[x] = (2·S[x], S[x], S[x], 3·S[x]) (rows 0..3, LE) and
+// its rotations T1..T3 (by 8/16/24 bits), each held in shared memory 32 times, interleaved
+// so that entry x of copy `lane` sits at byte offset x*128 + lane*4: every lane reads its
+// own copy, i.e. its own bank, so the 16 lookups of an AES round are conflict-free whatever
+// the state bytes are, and a column is four lookups XORed with no rotates. S[x] is byte 1
+// of T0[x] (for AESENCLAST). PH_STR_T1 = 0 keeps T0 only (rotates in the round), 1 keeps
+// T0 and T1. With 4 tables (128 KiB) one 1024-thread CTA per SM holds them once: config 4
+// ran 9.39 ms against 9.63 (2 tables) and 11.41 ms (1 table, 4 x 256 threads per SM).
 // init[len] caches the state after the first AESENC of aes_core for len < kInitLens: it
 // depends only on (len, seed), hash.cpp:120-122.
+#ifndef PH_STR_T1
+#define PH_STR_T1 2
+#endif
 constexpr uint32_t kInitLens = 256;
 struct AesTables {
     uint32_t t0[256 * 32];         // 32 KiB
+#if PH_STR_T1
+    uint32_t t1[256 * 32];         // T1 = T0 rotated by 8 bits, same interleave (32 KiB)
+#endif
+#if PH_STR_T1 > 1
+    uint32_t t2[256 * 32];         // T0 rotated by 16 bits
+    uint32_t t3[256 * 32];         // T0 rotated by 24 bits
+#endif
     uint4 init[kInitLens];         // 4 KiB
 };
 
@@ -63,6 +76,13 @@ __device__ void fill_tables(AesTables& T) {
         const uint8_t s = c_sbox[x];
         const uint8_t s2 = xtime(s), s3 = (uint8_t)(s2 ^ s);
         T.t0[e] = (uint32_t)s2 | ((uint32_t)s << 8) | ((uint32_t)s << 16) | ((uint32_t)s3 << 24);
+#if PH_STR_T1
+        T.t1[e] = __funnelshift_l(T.t0[e], T.t0[e], 8);
+#endif
+#if PH_STR_T1 > 1
+        T.t2[e] = __funnelshift_l(T.t0[e], T.t0[e], 16);
+        T.t3[e] = __funnelshift_l(T.t0[e], T.t0[e], 24);
+#endif
     }
 }
 
@@ -76,6 +96,16 @@ __device__ __forceinline__ uint32_t tk(uint32_t tb, uint32_t w) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"((byte << 7) + tb));
     return v;
 }
+#if PH_STR_T1
+// the same lookup in table TABLE (T1..T3, TABLE x 32 KiB after T0)
+template <int K, int TABLE = 1>
+__device__ __forceinline__ uint32_t tk1(uint32_t tb, uint32_t w) {
+    uint32_t byte, v;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(byte) : "r"(w), "n"(0x4440 + K));
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"((byte << 7) + tb), "n"(TABLE * 32768));
+    return v;
+}
+#endif
 
 // state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
 // in-memory byte order of the __m128i in hash.cpp. AESENC = ShiftRows,
@@ -84,12 +114,28 @@ __device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4],
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
+#if PH_STR_T1 > 1
+        const uint32_t a0 = tk<0>(tb, s[c]);
+        const uint32_t a1 = tk1<1, 1>(tb, s[(c + 1) & 3]);
+        const uint32_t a2 = tk1<2, 2>(tb, s[(c + 2) & 3]);
+        const uint32_t a3 = tk1<3, 3>(tb, s[(c + 3) & 3]);
+        o[c] = a0 ^ a1 ^ a2 ^ a3 ^ k[c];
+#elif PH_STR_T1
+        // T0[b0] ^ T1[b1] ^ rot16(T0[b2] ^ T1[b3]): one rotate per column instead of three
+        const uint32_t a0 = tk<0>(tb, s[c]);
+        const uint32_t a1 = tk1<1>(tb, s[(c + 1) & 3]);
+        const uint32_t a2 = tk<2>(tb, s[(c + 2) & 3]);
+        const uint32_t a3 = tk1<3>(tb, s[(c + 3) & 3]);
+        const uint32_t hi = a2 ^ a3;
+        o[c] = a0 ^ a1 ^ __funnelshift_l(hi, hi, 16) ^ k[c];
+#else
         const uint32_t a0 = tk<0>(tb, s[c]);
         const uint32_t a1 = tk<1>(tb, s[(c + 1) & 3]);
         const uint32_t a2 = tk<2>(tb, s[(c + 2) & 3]);
         const uint32_t a3 = tk<3>(tb, s[(c + 3) & 3]);
         o[c] = a0 ^ __funnelshift_l(a1, a1, 8) ^ __funnelshift_l(a2, a2, 16) ^
                __funnelshift_l(a3, a3, 24) ^ k[c];
+#endif
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
@@ -269,9 +315,18 @@ __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_
 // the same number of rounds; outputs go back to their input positions.
 constexpr int kBatchPer = 4;
 constexpr int kBatch = 32 * kBatchPer;
-constexpr int kBytesThreads = 256;
+#ifndef PH_STR_THREADS
+#define PH_STR_THREADS 1024  // one CTA per SM (registers), one copy of the tables per SM
+#endif
+constexpr int kBytesThreads = PH_STR_THREADS;
 constexpr int kBytesWarps = kBytesThreads / 32;
 constexpr uint32_t kClasses = 8;  // block counts 0..6, and 7 for >= 7 blocks
+
+struct BytesSmem {  // dynamic shared memory of k_query_bytes
+    AesTables T;
+    uint64_t off[kBytesWarps][kBatch + 1];  // each warp batch's offsets
+    uint8_t perm[kBytesWarps][kBatch];      // the batch in block-count order
+};
 
 template <int G, bool POW2, class OutT>
 __global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix,
@@ -279,9 +334,11 @@ __global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix
                                                      const uint64_t* __restrict__ offsets,
                                                      uint64_t base_off, OutT* __restrict__ out, uint64_t nkeys,
                                                      int minimal) {
-    __shared__ AesTables T;
-    __shared__ uint64_t s_off[kBytesWarps][kBatch + 1];
-    __shared__ uint8_t s_perm[kBytesWarps][kBatch];
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    BytesSmem& SM = *reinterpret_cast<BytesSmem*>(smem_raw);
+    AesTables& T = SM.T;
+    auto& s_off = SM.off;
+    auto& s_perm = SM.perm;
     const int algo = ix.hash_algo;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1;
@@ -382,15 +439,18 @@ template <int G, bool POW2, class OutT>
 static cudaError_t launch_b(const DevIndex& ix, const uint8_t* d, const uint64_t* o,
                             uint64_t bo, void* out, uint64_t n, int minimal, cudaStream_t s, int sms) {
     auto kern = k_query_bytes<G, POW2, OutT>;
+    constexpr size_t smem = sizeof(BytesSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int bps = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kBytesThreads, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kBytesThreads, smem) != cudaSuccess ||
         bps <= 0)
         bps = 1;
     const uint64_t want = (n + (uint64_t)kBatch * kBytesWarps - 1) / ((uint64_t)kBatch * kBytesWarps);
     const uint64_t cap = (uint64_t)sms * bps;
     const int blocks = (int)(want < cap ? want : cap);
     const cudaError_t e =
-        launch_ex(ix, kern, blocks, kBytesThreads, s, ix, d, o, bo, static_cast<OutT*>(out), n, minimal);
+        launch_ex_smem(ix, kern, blocks, kBytesThreads, smem, s, ix, d, o, bo, static_cast<OutT*>(out), n,
+                       minimal);
     note_launch();
     return e;
 }

@@ -47,29 +47,66 @@ __constant__ uint8_t c_sbox[256] = {
 // the state bytes are, and a column is four lookups XORed with no rotates. S[x] is byte 1
 // of T0[x] (for AESENCLAST). PH_STR_T1 = 0 keeps T0 only (rotates in the round), 1 keeps
 // T0 and T1. With 4 tables (128 KiB) one 1024-thread CTA per SM holds them once: config 4
-// ran 9.39 ms against 9.63 (2 tables) and 11.41 ms (1 table, 4 x 256 threads per SM).
+// ran 9.39 ms against 9.63 (2 tables) and 11.41 ms (1 table, 4 x 256 threads per SM), and
+// 9.13 ms with the PRMT-formed addresses below.
 // init[len] caches the state after the first AESENC of aes_core for len < kInitLens: it
 // depends only on (len, seed), hash.cpp:120-122.
 #ifndef PH_STR_T1
 #define PH_STR_T1 2
 #endif
 constexpr uint32_t kInitLens = 256;
+#if PH_STR_T1 > 1
+// Four tables in two 64 KiB halves: entry x of table t for lane l sits at byte
+// (t>>1)*64 KiB + x*256 + (t&1)*128 + l*4, so that one PRMT forms x*256 + l*4 (byte K of the
+// state word into byte 1, the lane offset into byte 0) and the table is an immediate offset.
+struct AesTables {
+    uint32_t t[4 * 256 * 32];      // 128 KiB
+    uint4 init[kInitLens];         // 4 KiB
+};
+#else
 struct AesTables {
     uint32_t t0[256 * 32];         // 32 KiB
 #if PH_STR_T1
     uint32_t t1[256 * 32];         // T1 = T0 rotated by 8 bits, same interleave (32 KiB)
 #endif
-#if PH_STR_T1 > 1
-    uint32_t t2[256 * 32];         // T0 rotated by 16 bits
-    uint32_t t3[256 * 32];         // T0 rotated by 24 bits
-#endif
     uint4 init[kInitLens];         // 4 KiB
 };
+#endif
 
 __device__ __forceinline__ uint8_t xtime(uint8_t a) {
     return (uint8_t)((a << 1) ^ ((a & 0x80) ? 0x1b : 0));
 }
 
+__device__ __forceinline__ uint32_t t0_entry(int x) {
+    const uint8_t s = c_sbox[x];
+    const uint8_t s2 = xtime(s), s3 = (uint8_t)(s2 ^ s);
+    return (uint32_t)s2 | ((uint32_t)s << 8) | ((uint32_t)s << 16) | ((uint32_t)s3 << 24);
+}
+
+#if PH_STR_T1 > 1
+extern __shared__ __align__(16) uint8_t smem_raw[];  // BytesSmem, AesTables first
+__device__ __forceinline__ uint32_t tables_base() {
+    return (uint32_t)__cvta_generic_to_shared(smem_raw);
+}
+__device__ void fill_tables(AesTables& T) {
+    for (int e = threadIdx.x; e < 4 * 256 * 32; e += blockDim.x) {
+        const int t = e >> 13, x = (e >> 5) & 255, l = e & 31;
+        const uint32_t v = t0_entry(x);
+        T.t[((t >> 1) << 14) + (x << 6) + ((t & 1) << 5) + l] = __funnelshift_l(v, v, 8 * t);
+    }
+}
+// Lookup of table TABLE at byte K of w in this lane's copy: PRMT forms byte*256 + lane*4
+// (lw = lane*4, bytes 1..3 zero), LDS reads it at the table's constant offset -- two
+// instructions per lookup. base = shared-window address of T.t.
+template <int K, int TABLE>
+__device__ __forceinline__ uint32_t tq(uint32_t base, uint32_t lw, uint32_t w) {
+    uint32_t a, v;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(a) : "r"(w), "r"(lw), "n"(0x5504 | (K << 4)));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v)
+                 : "r"(base + a + (uint32_t)((TABLE >> 1) * 65536 + (TABLE & 1) * 128)));
+    return v;
+}
+#else
 __device__ void fill_tables(AesTables& T) {
     for (int e = threadIdx.x; e < 256 * 32; e += blockDim.x) {
         const int x = e >> 5;
@@ -79,13 +116,21 @@ __device__ void fill_tables(AesTables& T) {
 #if PH_STR_T1
         T.t1[e] = __funnelshift_l(T.t0[e], T.t0[e], 8);
 #endif
-#if PH_STR_T1 > 1
-        T.t2[e] = __funnelshift_l(T.t0[e], T.t0[e], 16);
-        T.t3[e] = __funnelshift_l(T.t0[e], T.t0[e], 24);
-#endif
     }
 }
+#endif
 
+#if PH_STR_T1 > 1
+// tb = lane*4 here
+template <int K>
+__device__ __forceinline__ uint32_t tk(uint32_t tb, uint32_t w) {
+    return tq<K, 0>(tables_base(), tb, w);
+}
+template <int K, int TABLE = 1>
+__device__ __forceinline__ uint32_t tk1(uint32_t tb, uint32_t w) {
+    return tq<K, TABLE>(tables_base(), tb, w);
+}
+#else
 // Lookup of T0[byte k of w] in this lane's copy: PRMT extracts byte k, LEA forms
 // byte*128 + (this lane's table base), LDS reads it -- three instructions per lookup.
 // tb = shared-window address of T.t0 plus lane*4.
@@ -105,6 +150,7 @@ __device__ __forceinline__ uint32_t tk1(uint32_t tb, uint32_t w) {
     asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"((byte << 7) + tb), "n"(TABLE * 32768));
     return v;
 }
+#endif
 #endif
 
 // state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
@@ -342,7 +388,11 @@ __global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix
     const int algo = ix.hash_algo;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1;
+#if PH_STR_T1 > 1
+    const uint32_t tb = lane * 4;
+#else
     const uint32_t tb = (uint32_t)__cvta_generic_to_shared(T.t0) + lane * 4;
+#endif
     if (algo == 1 || algo == 2) {
         fill_tables(T);
         __syncthreads();

@@ -520,6 +520,12 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
         d.magic_hi = static_cast<uint64_t>(m >> 64);
         d.magic_lo = static_cast<uint64_t>(m);
         d.mod_m64 = static_cast<uint64_t>((u128{1} << 64) / p.S);
+        const phg::ModFast mf = phg::mod_fast_make(p.S);  // same remainder, 32-bit products
+        d.mod_fast_ok = mf.ok && !std::getenv("PH_GPU_NO_MODFAST");
+        d.mod_nS = mf.nS;
+        d.mod_c = mf.c;
+        d.mod_m1 = mf.m1;
+        d.mod_m2 = mf.m2;
     }
     d.hp_base = phg::kC * (p.seed & ~uint64_t{0xff});
     d.seed_lo8 = static_cast<uint32_t>(p.seed & 0xff);

@@ -146,9 +146,9 @@ __global__ void __launch_bounds__(256) k_bucket_count(const DevIndex ix,
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t h = kC * (keys[i] ^ ix.seed);  // hash_int, hash.hpp:27
-        uint64_t x, unused;
+        uint64_t x;
         const uint32_t part = (uint32_t)mul32x64(P32, h, x);  // part_and_bucket, bucket_fn.hpp:66-72
-        const uint32_t bucket = (uint32_t)mul32x64(B32, gamma<G>(x, ix.opt_table), unused);
+        const uint32_t bucket = bucket_of<G>(x, B32, ix.opt_table);
         atomicAdd(cnt + (uint64_t)part * B32 + bucket, 1u);
     }
 }

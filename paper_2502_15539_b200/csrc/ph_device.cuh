@@ -13,6 +13,12 @@
 
 #include <cstdint>
 
+#include "ph_arith.cuh"
+
+#ifndef PH_NO_FAST_BUCKET
+#define PH_NO_FAST_BUCKET 1  // 0: bucket_fast with the exact form out of line (A/B builds)
+#endif
+
 namespace phg {
 
 constexpr uint64_t kC = 0x517cc1b727220a95ULL;  // hash.hpp:13
@@ -31,6 +37,10 @@ struct DevIndex {
     uint64_t mod_m64;             // floor(2^64 / S) for the device's exact y mod S
     uint64_t hp_base;             // C * (seed & ~0xff): hash_pilot(p) = hp_base + C*((seed^p)&0xff)
     uint32_t seed_lo8;
+    // mod_fast constants (ph_arith.cuh) when 2^13 <= S < 2^21 (mod_fast_ok), else the
+    // 64-bit form via mod_m64
+    uint32_t mod_nS, mod_c, mod_m1, mod_m2;  // mod_nS = -S mod 2^32
+    int32_t mod_fast_ok;
     int32_t remap_kind;           // 0 plain32, 1 CacheLineEF, 2 Elias-Fano
     int32_t ef_low_bits;
     int32_t hash_algo;
@@ -148,7 +158,9 @@ __device__ __forceinline__ uint64_t gamma(uint64_t x, const uint64_t* __restrict
 // ---------------------------------------------------------------------------
 // reduce, reduce.hpp:38-43 / :67-70
 // ---------------------------------------------------------------------------
-template <bool POW2>
+// MF: 1 = mod_fast (the caller checked ix.mod_fast_ok), 0 = the 64-bit form, -1 = decide
+// from ix.mod_fast_ok at run time (a uniform branch).
+template <bool POW2, int MF = -1>
 __device__ __forceinline__ uint64_t reduce(const DevIndex& ix, uint64_t y) {
     if constexpr (POW2) {
         return mulhi(kC, y) & (ix.S - 1);
@@ -157,9 +169,36 @@ __device__ __forceinline__ uint64_t reduce(const DevIndex& ix, uint64_t y) {
         // 128-bit-magic bound; verified against 128-bit division in tests/test_oracle.py).
         // Same value, fewer multiplies: q = hi64(y * floor(2^64/S)) is floor(y/S) or one
         // less, so r = y - q*S lies in [0, 2S) and one conditional subtract finishes it.
+        // For 2^13 <= S < 2^21 (every config) mod_fast gives the same value with 32-bit
+        // products only (ph_arith.cuh); the branch is on a kernel parameter (uniform).
+        if (MF == 1 || (MF == -1 && ix.mod_fast_ok))
+            return mod_fast(y, (uint32_t)ix.S, ix.mod_nS, ix.mod_c, ix.mod_m1, ix.mod_m2);
         const uint64_t q = mulhi(y, ix.mod_m64);
         uint64_t r = y - q * (uint32_t)ix.S;
         return r >= ix.S ? r - ix.S : r;
+    }
+}
+
+// bucket = hi64(B * gamma(x)) (bucket_fn.hpp:66-72), B < 2^32. For the polynomial bucket
+// functions (linear, quadratic, cubic) bucket_fast brackets gamma from the top word of x
+// and is exact for all but ~B*10/2^32 of the keys; those take the 64-bit form out of line.
+template <int G>
+static __device__ __noinline__ uint32_t bucket_exact(uint64_t x, uint32_t B,
+                                                     const uint64_t* __restrict__ opt) {
+    uint64_t unused;
+    return (uint32_t)mul32x64(B, gamma<G>(x, opt), unused);
+}
+template <int G>
+__device__ __forceinline__ uint32_t bucket_of(uint64_t x, uint32_t B,
+                                              const uint64_t* __restrict__ opt) {
+    if constexpr (G <= 2 && !PH_NO_FAST_BUCKET) {
+        bool ok;
+        const uint32_t b = bucket_fast<G>((uint32_t)(x >> 32), B, ok);
+        if (__builtin_expect(ok, 1)) return b;
+        return bucket_exact<G>(x, B, opt);
+    } else {
+        uint64_t unused;
+        return (uint32_t)mul32x64(B, gamma<G>(x, opt), unused);
     }
 }
 

@@ -215,6 +215,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -545,12 +548,12 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
     if (tid == 0) bulk_wait_all();
 }
 
-// Pass B: the query arithmetic over the group regions (region r < G: group r, r == G: the
-// spill), non-minimal slots into slots[] at the same entry index (remap_slot happens in
-// pass C). CTAs claim batches of 2048-entry chunks in order from a global counter, so the
-// chunks in flight always form one contiguous window (one or two regions): the current
-// pilot slice stays L2-resident. Dynamic claiming also keeps the pass balanced when it shares the SMs
-// with another chunk's pass A or C.
+// Pass B: the query arithmetic, remap_slot included, over the group regions (region r < G:
+// group r, r == G: the spill); slots[] gets each entry's answer at the same entry index.
+// CTAs claim batches of 2048-entry chunks in order from a global counter, so the chunks in
+// flight always form one contiguous window (one or two regions): the current pilot slice
+// stays L2-resident. (Measured and not kept: each chunk's entries bulk-copied into shared
+// memory a chunk ahead by a producer thread, 5.40 vs 5.22 ms at config 3.)
 constexpr int kQThreads = 256;
 #ifndef PH_QB_PER
 #define PH_QB_PER 8
@@ -564,7 +567,7 @@ constexpr uint32_t kQChunk = kQThreads * kQPer;       // 2048 entries per chunk
 #define PH_QB_CLAIM 8  // chunks per claim, one CTA barrier per claim (1, 2, 4, 8, 16, 32 swept: 8-16 best, ~1 %)
 #endif
 
-template <int G, bool POW2, class OutT>
+template <int G, bool POW2, class OutT, int MF>
 __global__ void __launch_bounds__(kQThreads, PH_QB_MINB) k_query_regions(
     const DevIndex ix, uint32_t NG, uint64_t cap, unsigned long long* __restrict__ ctrl,
     const uint64_t* __restrict__ bins, OutT* __restrict__ slots, int minimal) {
@@ -611,16 +614,16 @@ __global__ void __launch_bounds__(kQThreads, PH_QB_MINB) k_query_regions(
 #pragma unroll
         for (int j = 0; j < kQPer; j++) {
             h[j] = kC * (h[j] ^ ix.seed);  // hash_int, hash.hpp:27
-            uint64_t x, unused;
+            uint64_t x;
             part[j] = (uint32_t)mul32x64(P32, h[j], x);  // part_and_bucket, bucket_fn.hpp:66-72
-            const uint32_t bucket = (uint32_t)mul32x64(B32, gamma<G>(x, ix.opt_table), unused);
+            const uint32_t bucket = bucket_of<G>(x, B32, ix.opt_table);
             pilot[j] = ld_gather_u8(ix.pilots + ((uint64_t)part[j] * B32 + bucket), pol_keep);
         }
         uint64_t slot[kQPer];
         bool need[kQPer];
 #pragma unroll
         for (int j = 0; j < kQPer; j++) {  // slot_of, index.hpp:91-96
-            slot[j] = (uint64_t)part[j] * S32 + reduce<POW2>(ix, h[j] ^ hash_pilot(ix, pilot[j]));
+            slot[j] = (uint64_t)part[j] * S32 + reduce<POW2, MF>(ix, h[j] ^ hash_pilot(ix, pilot[j]));
             const uint64_t e = e0 + ((uint64_t)(j >> 1) * kQThreads + tid) * 2 + (j & 1);
             need[j] = minimal && slot[j] >= ix.n && e < end;
         }
@@ -655,8 +658,9 @@ static cudaError_t launch_regions(const DevIndex& ix, int gamma_kind, bool pow2,
     const int grid = (int)std::min<uint64_t>(chunks_max, (uint64_t)sms * per_sm);
 #define PH_CASE(GK)                                                                              \
     case GK:                                                                                     \
-        if (pow2) k_query_regions<GK, true, OutT><<<grid, kQThreads, 0, s>>>(ix, G, cap, ctrl, bins, slots, minimal); \
-        else k_query_regions<GK, false, OutT><<<grid, kQThreads, 0, s>>>(ix, G, cap, ctrl, bins, slots, minimal);    \
+        if (pow2) k_query_regions<GK, true, OutT, 0><<<grid, kQThreads, 0, s>>>(ix, G, cap, ctrl, bins, slots, minimal); \
+        else if (ix.mod_fast_ok) k_query_regions<GK, false, OutT, 1><<<grid, kQThreads, 0, s>>>(ix, G, cap, ctrl, bins, slots, minimal); \
+        else k_query_regions<GK, false, OutT, 0><<<grid, kQThreads, 0, s>>>(ix, G, cap, ctrl, bins, slots, minimal);    \
         break;
     switch (gamma_kind) {
         PH_CASE(0)

@@ -181,8 +181,7 @@ __global__ void __launch_bounds__(PH_THREADS, MINB) k_query_u64(const DevIndex i
             // part_and_bucket, bucket_fn.hpp:66-72 (P, B < 2^32: checked at create)
             uint64_t x;
             part[j] = (uint32_t)mul32x64(P32, h[j], x);
-            uint64_t unused;
-            const uint32_t bucket = (uint32_t)mul32x64(B32, gamma<G>(x, ix.opt_table), unused);
+            const uint32_t bucket = bucket_of<G>(x, B32, ix.opt_table);
             if (HOTF) {
                 const bool hot = bucket < ix.hot_b;
                 pilot[j] = ld_gather_u8(ix.pilots + pilot_offset(ix, part[j], bucket),

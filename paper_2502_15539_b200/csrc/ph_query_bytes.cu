@@ -462,8 +462,9 @@ __global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix
                     hi = lo = portable_hash64(data, o0, len, ix.seed);
                 }
             }
-            const uint64_t part = mulhi(ix.P, hi);
-            const uint64_t bucket = mulhi(ix.B, gamma<G>(ix.P * hi, ix.opt_table));
+            uint64_t x;
+            const uint64_t part = mul32x64((uint32_t)ix.P, hi, x);  // P, B < 2^32 (create)
+            const uint64_t bucket = bucket_of<G>(x, (uint32_t)ix.B, ix.opt_table);
             const bool hot = bucket < ix.hot_b;
             const uint32_t pilot =
                 valid ? ld_gather_u8(ix.pilots + pilot_offset(ix, part, bucket),

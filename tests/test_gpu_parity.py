@@ -116,6 +116,31 @@ def test_fresh_index_vs_reference(ph, ref, preset, over):
     assert np.array_equal(np.sort(got), np.arange(n, dtype=np.uint64))
 
 
+@pytest.mark.parametrize("slots_target", [6000, 9000, 300_000, 2_200_000])
+def test_mod_fast_and_64bit_reduce_agree(ph, ref, slots_target, monkeypatch):
+    """y mod S by the 32-bit form (ph_arith.cuh mod_fast, 2^13 <= S < 2^21) and by the 64-bit
+    form (PH_GPU_NO_MODFAST) on the same index: both equal the reference (reduce.hpp:38-43).
+    S straddles the fast form's range (one part of ~slots_target slots)."""
+    from oracle.bindings import corpus_u64_np
+    n = int(slots_target * 0.99)
+    keys = corpus_u64_np(0, n, 31)
+    S = slots_target
+    ptrh = ref.build_u64_shape(keys, ref.params("default", lambda_=(30, 10)), 1, S,
+                               max(1, n // 3))
+    ri = ref.load(ptrh)
+    q = np.concatenate([keys, corpus_u64_np(0, n, 32)])
+    outs = []
+    for off in ("", "1"):
+        if off:
+            monkeypatch.setenv("PH_GPU_NO_MODFAST", off)
+        idx = ph.PtrHashIndex(ptrh)
+        outs.append([gpu_query(idx, q, m, 8) for m in (True, False)])
+        idx.close()
+    for m, got_fast, got_slow in zip((True, False), outs[0], outs[1]):
+        want = ri.query_u64(q, m, "loop", threads=THREADS)
+        assert np.array_equal(got_fast, want) and np.array_equal(got_slow, want)
+
+
 def test_config1_full_bijective_and_bitexact(ph, ref):
     """BASELINE config 1: n=1e7, λ=3.0, α=0.99, cubic, CacheLineEF, shuffled, u32 out."""
     from oracle.bindings import corpus_u64_np

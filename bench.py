@@ -209,6 +209,36 @@ def build_index_bytes(n: int, dist: Dist, gen_keys, build=None, tag="u64") -> by
     return ptrh
 
 
+def ptrh_shape(ptrh: bytes) -> dict:
+    """n, P, S, B and the query-relevant ids from a PTRH v1 header (serde.hpp:12-31)."""
+    import struct
+    key_kind, algo, fn, remap, reduce_ = ptrh[8], ptrh[9], ptrh[10], ptrh[11], ptrh[12]
+    n, P, S, B = struct.unpack_from("<QQQQ", ptrh, 16)
+    return {"n": n, "P": P, "S": S, "B": B, "hash": algo, "bucket_fn": fn, "remap": remap,
+            "key_kind": key_kind, "reduce": reduce_}
+
+
+def config_dict(cfg: dict, ptrh: bytes, world: int) -> dict:
+    """The workload as both arms print it (the driver compares the two `config`s)."""
+    sh = ptrh_shape(ptrh)
+    return {"workload": cfg["desc"], "n": sh["n"], "queries_per_step_per_gpu": cfg["nq"],
+            "params": "preset default, lambda=3.0, alpha=0.99, cubic gamma, CacheLineEF, "
+                      "fastmod S",
+            "P": sh["P"], "S": sh["S"], "B": sh["B"], "hash": sh["hash"],
+            "output": "u32, minimal", "parallelism": f"replicas x{world} (no collective)"}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -278,12 +308,15 @@ class U64Work:
         qh = self.pin_q.numpy().view(np.uint64)[:m]
         return ri.query_u64(qh, minimal, "stream", 32, threads=os.cpu_count() or 1)
 
-    def cpu_sample(self, ri, S):
+    def cpu_runner(self, ri, S):
+        """run(count, minimal, mode, width, threads): the reference's bulk query over the
+        first `count` queries of this stream (host copy, untimed)."""
         sample = np.ascontiguousarray(self.pin_q.numpy().view(np.uint64)[:S])
         out = np.empty(S, dtype=np.uint64)
-        T = os.cpu_count() or 1
-        return (lambda: ri.query_u64(sample, True, "stream", 32, threads=T, out=out)), \
-            f"first {S} queries of the same stream, index_stream lookahead 32, minimal, {T} threads"
+
+        def run(count, minimal, mode, width, threads):
+            ri.query_u64(sample[:count], minimal, mode, width, threads=threads, out=out[:count])
+        return run, "queries of the same shuffled stream", lambda: None
 
 
 class StrWork:
@@ -349,14 +382,25 @@ class StrWork:
         o = self.pin_offs.numpy().view(np.uint64)[:m + 1]
         return ri.query_bytes(d, o, minimal, "single", threads=os.cpu_count() or 1)
 
-    def cpu_sample(self, ri, S):
+    def cpu_runner(self, ri, S):
+        """The reference's span<const std::string> bulk queries over std::strings made once
+        from the first S queries of the stream (materialisation untimed)."""
+        from oracle.bindings import RefStrings
         d = self.pin_data.numpy()
         o = np.ascontiguousarray(self.pin_offs.numpy().view(np.uint64)[:S + 1])
+        sets = {}
         out = np.empty(S, dtype=np.uint64)
-        T = os.cpu_count() or 1
-        return (lambda: ri.query_bytes(d, o, True, "single", threads=T, out=out)), \
-            (f"first {S} queries of the same shuffled stream, reference index(string_view) over "
-             f"the concatenated buffer (std::string materialisation avoided), minimal, {T} threads")
+
+        def run(count, minimal, mode, width, threads):
+            if count not in sets:
+                sets[count] = RefStrings(ri.ref, d, o[:count + 1])
+            sets[count].query(ri, minimal, mode, width, threads=threads, out=out[:count])
+
+        def close():
+            for v in sets.values():
+                v.close()
+        return run, ("queries of the same shuffled stream as std::string keys "
+                     "(materialised before timing)"), close
 
 
 class KmerWork:
@@ -417,14 +461,14 @@ class KmerWork:
         kh = self.kmers_host.numpy().view(np.uint64)[:m]
         return ri.query_u64(kh, minimal, "stream", 32, threads=os.cpu_count() or 1)
 
-    def cpu_sample(self, ri, S):
+    def cpu_runner(self, ri, S):
         sample = np.ascontiguousarray(self.kmers_host.numpy().view(np.uint64)[:S])
         out = np.empty(S, dtype=np.uint64)
-        T = os.cpu_count() or 1
-        return (lambda: ri.query_u64(sample, True, "stream", 32, threads=T, out=out)), \
-            (f"first {S} k-mers in sequence order, materialised as u64 keys (the reference has "
-             f"no k-mer front end; extraction untimed), index_stream lookahead 32, minimal, "
-             f"{T} threads")
+
+        def run(count, minimal, mode, width, threads):
+            ri.query_u64(sample[:count], minimal, mode, width, threads=threads, out=out[:count])
+        return run, ("k-mers in sequence order, materialised as u64 keys (the reference has no "
+                     "k-mer front end; extraction untimed)"), lambda: None
 
 
 WORKLOADS = {"u64": U64Work, "str": StrWork, "kmer": KmerWork}
@@ -579,41 +623,81 @@ def run_ours(args, cfg):
     if not torch.equal(pin_o.cuda(), out):
         raise SystemExit("e2e host-path output differs from the device path")
 
+    # ---- replay bound: the pilot gathers alone at the true bucket addresses ----
+    replay = replay_bounds(W, idx, info, time_ms, cfg, args)
+
     # ---- report ----
     N, K = dist.world, args.steps
     value = N * nq * K / (total_ms * 1e-3) / 1e9
-    kern_ms = statistics.mean(ms_min)
+    step_ms = total_ms / K
     sectors = 1.0 + remap_frac * (1.0 + 32.0 / 44.0)  # pilot + CLEF (i>=12 touches 2nd sector)
-    # Pilots + remap table that fit in L2 (the partitioned path's 64 MiB threshold) come from
-    # DRAM once per step (L2 is flushed between steps); beyond that every gather is a DRAM sector.
     table_bytes = int(info.pilot_bytes) + int(info.remap_bytes)
-    l2_resident = table_bytes <= (64 << 20)
-    if l2_resident:
+    peak, peak_src = measured_peaks()
+    in_bytes = W.stream_bytes - 4.0  # keys (8 B), packed bases (0.25 B) or string bytes+offsets
+    partitioned = passes is not None
+    if partitioned:
+        # The path as built: pass A reads the input and writes (key, position)
+        # entries (10 B), pass B reads the keys (8 B) and writes u32 slots (4 B), pass C reads
+        # (slot, position) (6 B) and writes the output (4 B); the pilots and the remap table
+        # come from DRAM once per step (their slices are L2-resident while pass B runs).
+        per_key = {"A": in_bytes + 10.0, "B": 12.0, "C": 10.0}
+        bytes_per_key = sum(per_key.values()) + table_bytes / nq
+        dram_note = (f"path as built: pass A {per_key['A']:.2f} B (input + 10 B entry) + pass B "
+                     f"12 B (8 B key + 4 B slot) + pass C 10 B (6 B entry + 4 B out) per query "
+                     f"+ pilots and remap once per step ({table_bytes} B)")
+    elif table_bytes <= (64 << 20):
         bytes_per_key = W.stream_bytes + table_bytes / nq
         dram_note = (f"{W.stream_bytes:.2f} B streamed per query + the L2-resident pilots and "
-                     f"remap table read once per step ({table_bytes} B / {nq} queries); the "
-                     f"binding bound is the L2 gather rate (gather_roofline)")
+                     f"remap table once per step ({table_bytes} B); the binding bound is the L2 "
+                     f"gather rate (dominant_kernel)")
     else:
         bytes_per_key = W.stream_bytes + 32.0 * sectors
         dram_note = (f"{W.stream_bytes:.2f} B streamed per query + 32 B x (1 pilot sector + "
-                     f"remap_fraction x 1.727 CacheLineEF sectors)")
-    peak, peak_src = measured_peaks()
-    achieved = nq * bytes_per_key / (kern_ms * 1e-3) / 1e9
+                     f"remap_fraction x 1.727 CacheLineEF sectors) from DRAM")
+    achieved = nq * bytes_per_key / (step_ms * 1e-3) / 1e9
     stream_ms = nq * W.stream_bytes / (bw_copy * 1e9) * 1e3
     gather_ms = nq * sectors / (r_gather * 1e9) * 1e3
-    t_roof = max(stream_ms, gather_ms)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as f:
-                traffic = json.load(f).get(f"config{args.config}", {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    t_model = max(stream_ms, gather_ms)
+    traffic, traffic_src = measured_traffic(args.config)
     cpu = None
     if dist.rank == 0 and N == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(W, args)
-    bin_bytes = (W.stream_bytes - 4.0) + 10.0  # keys (or packed bases) in; key + position out
+    dominant = None
+    pass_block = None
+    if partitioned:
+        A, B, Cc = passes
+        gathers_b = nq * sectors / (B * 1e-3) / 1e9
+        pass_block = {
+            "method": "CUDA events around the three passes on the query stream "
+                      "(ph_gpu_set_pass_timing), mean over a separate loop of the same steps",
+            "bin": {"kernel": "k_bin_tma", "ms": round(A, 4), "bound": "hbm",
+                    "algorithmic_bytes_per_key": round(per_key["A"], 3),
+                    "achieved_gbs": round(nq * per_key["A"] / A / 1e6, 1),
+                    "frac": round(nq * per_key["A"] / A / 1e6 / peak, 4)},
+            "query": {"kernel": "k_query_regions", "ms": round(B, 4),
+                      "bound": "L1->XBAR request port: one L2 request per pilot gather from "
+                               "the L2-resident slice",
+                      "gathers_gsectors_s": round(gathers_b, 2),
+                      "peak_gsectors_s": round(r_gather_slice, 2),
+                      "peak_source": f"live k_gather microbenchmark over {slice_bytes >> 20} MiB",
+                      "frac": round(gathers_b / r_gather_slice, 4),
+                      "hbm_bytes_per_key": 12.0,
+                      "hbm_frac": round(nq * 12.0 / B / 1e6 / peak, 4)},
+            "unbin": {"kernel": "k_unbin_tma", "ms": round(Cc, 4), "bound": "hbm",
+                      "algorithmic_bytes_per_key": 10.0,
+                      "achieved_gbs": round(nq * 10.0 / Cc / 1e6, 1),
+                      "frac": round(nq * 10.0 / Cc / 1e6 / peak, 4)},
+        }
+        k = max(("bin", "query", "unbin"), key=lambda x: pass_block[x]["ms"])
+        pass_block["dominant"] = k
+        dominant = dict(pass_block[k], share_of_step=round(pass_block[k]["ms"] / step_ms, 4))
+    elif table_bytes <= (64 << 20) and cfg["kind"] != "str":
+        dominant = {"kernel": "k_query_u64", "ms": round(step_ms, 4),
+                    "bound": "L2 random gather (pilots L2-resident)",
+                    "gathers_gsectors_s": round(nq * sectors / step_ms / 1e6, 2),
+                    "peak_gsectors_s": round(r_gather, 2),
+                    "peak_source": f"live k_gather microbenchmark over {int(info.pilot_bytes)} B",
+                    "frac": round(nq * sectors / step_ms / 1e6 / r_gather, 4)}
     res = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -622,21 +706,17 @@ def run_ours(args, cfg):
         "n_gpus": N,
         "steps": K,
         "warmup": args.warmup,
-        "ms_per_step": round(total_ms / K, 4),
+        "ms_per_step": round(step_ms, 4),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic (seeded generators, SURVEY §8d; index built by the reference builder)",
-        "config": {"workload": cfg["desc"], "n": n, "queries_per_step_per_gpu": nq,
-                   "params": "preset default, lambda=3.0, alpha=0.99, cubic gamma, CacheLineEF, "
-                             "fastmod S", "P": int(info.parts), "S": int(info.slots_per_part),
-                   "B": int(info.buckets_per_part), "hash": int(info.hash_algo),
-                   "output": "u32, minimal", "parallelism": f"replicas x{N} (no collective)",
-                   "pilot_layout": ("file order, partitioned path" if cfg.get("layout") == "file"
-                                    else "hot-first + persisting window" if cfg.get("layout") == "hot"
-                                    else "library default (file order)"),
-                   "l2": "flushed between steps (512 MiB write, outside the timed events)"},
+        "config": config_dict(cfg, W.ptrh, N),
+        "setup": {"pilot_layout": ("file order, partitioned path" if partitioned
+                                   else "hot-first + persisting window" if cfg.get("layout") == "hot"
+                                   else "library default (file order)"),
+                  "l2": "flushed between steps (512 MiB write, outside the timed events)"},
         "nonminimal": {"value": round(N * nq * K / (total_nm * 1e-3) / 1e9, 3), "unit": "Gkeys/s",
                        "ms_per_step": round(total_nm / K, 4)},
         "gpu_launches": int(launches),
@@ -645,64 +725,170 @@ def run_ours(args, cfg):
                 "api": W.api, "gpu_launches": int(e2e_launches)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "scope": ("the whole query step (passes A+B+C)" if partitioned
+                               else "the query kernel"),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_key": round(bytes_per_key, 3),
-                     "note": dram_note},
-        "gather_roofline": {"t_roof_ms": round(t_roof, 4), "t_measured_ms": round(kern_ms, 4),
-                            "frac": round(t_roof / kern_ms, 4),
-                            "stream_bound_ms": round(stream_ms, 4),
-                            "gather_bound_ms": round(gather_ms, 4),
-                            "copy_gbs": round(bw_copy, 1),
-                            "r_gather_gsectors_s": round(r_gather, 3),
-                            "gather_buffer_bytes": int(info.pilot_bytes)},
-        "partition_passes": None if passes is None else {
-            "method": "CUDA events around the three passes on the query stream "
-                      "(ph_gpu_set_pass_timing), mean over a separate loop of the same steps",
-            "bin": {"kernel": "k_bin_tma", "ms": round(passes[0], 4),
-                    "bound": "hbm", "algorithmic_bytes_per_key": round(bin_bytes, 3),
-                    "achieved_gbs": round(nq * bin_bytes / passes[0] / 1e6, 1),
-                    "frac": round(nq * bin_bytes / passes[0] / 1e6 / peak, 4)},
-            "query": {"kernel": "k_query_regions", "ms": round(passes[1], 4),
-                      "bound": "L1TEX wavefronts / L2 tag lookups of the random pilot gather "
-                               "(one 32-B sector per key from an L2-resident slice)",
-                      "gathers_gsectors_s": round(nq * sectors / passes[1] / 1e6, 2),
-                      "peak_gsectors_s": round(r_gather_slice, 2),
-                      "peak_source": f"live k_gather microbenchmark over {slice_bytes >> 20} MiB",
-                      "frac": round(nq * sectors / passes[1] / 1e6 / r_gather_slice, 4),
-                      "stream_bytes_per_key": 12.0},
-            "unbin": {"kernel": "k_unbin_tma", "ms": round(passes[2], 4),
-                      "bound": "hbm", "algorithmic_bytes_per_key": 10.0,
-                      "achieved_gbs": round(nq * 10.0 / passes[2] / 1e6, 1),
-                      "frac": round(nq * 10.0 / passes[2] / 1e6 / peak, 4)},
-            "dominant": ["bin", "query", "unbin"][max(range(3), key=lambda i: passes[i])],
-        },
+                     "note": dram_note,
+                     "frac_vs_stream_floor": round(stream_ms / step_ms, 4),
+                     "stream_floor": f"{W.stream_bytes:.2f} B/query (input + u32 out) at the "
+                                     f"live copy bandwidth {bw_copy:.0f} GB/s: "
+                                     f"{stream_ms:.4f} ms"},
+        "dominant_kernel": dominant,
+        "uniform_gather_model": {
+            "what": "SURVEY §8d / BASELINE.md §2: max(stream bytes / copy bandwidth, pilot + "
+                    "remap sectors / uniform random-gather rate over the whole pilot array); "
+                    "the skewed cubic-gamma access and the partitioned path both beat it",
+            "t_model_ms": round(t_model, 4), "t_measured_ms": round(step_ms, 4),
+            "speedup_vs_model": round(t_model / step_ms, 4),
+            "additive_bound_ms": round(stream_ms + gather_ms, 4),
+            "stream_bound_ms": round(stream_ms, 4), "gather_bound_ms": round(gather_ms, 4),
+            "copy_gbs": round(bw_copy, 1), "r_gather_gsectors_s": round(r_gather, 3),
+            "gather_buffer_bytes": int(info.pilot_bytes)},
+        "replay": replay,
+        "partition_passes": pass_block,
         "gate": gate,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
     }
+    # free this config's device and pinned memory before the secondary configs run
+    del W, idx, out, out_nm, pin_o, flush
+    ph_gpu_trim_all()
+    if dist.rank == 0 and N == 1 and args.secondary_configs and args.config == 3:
+        res["secondary"] = run_secondaries(args)
     if dist.rank == 0:
         print(json.dumps(res), flush=True)
     dist.close()
 
 
-def cpu_baseline(W, args):
-    """The reference's CPU query on all host cores over a bounded sample of the same stream,
-    contiguous slices (proj/tools/ptrhash.cpp:486-512), one warm-up then best of 3
-    (:212-223)."""
-    from oracle.bindings import Ref
-    ri = Ref().load(W.ptrh)
-    S = min(W.nq, args.cpu_sample)
-    fn, desc = W.cpu_sample(ri, S)
+def ph_gpu_trim_all():
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def measured_traffic(config: int):
+    """DRAM bytes per step (dram__bytes_read.sum + dram__bytes_write.sum over the step's
+    kernels) from the committed ncu capture of this bench's own command on its own fixture
+    (profiles/r02_traffic.json, written by tools/traffic_from_ncu.py)."""
+    prof = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    try:
+        with open(prof) as f:
+            d = json.load(f).get(f"config{config}")
+        return int(d["dram_bytes_per_step"]), d["source"]
+    except Exception:
+        return None, None
+
+
+def replay_bounds(W, idx, info, time_ms, cfg, args):
+    """The pilot reads alone (ph_gpu_gather_replay_u64) at the index's true bucket addresses:
+    in query order (the direct kernel's access pattern) and, for the partitioned path, with
+    the keys stably sorted by partition group (pass B's access pattern). u64 / k-mer configs."""
+    import torch
+    keys = getattr(W, "q", None)
+    if cfg["kind"] == "kmer":
+        keys = torch.from_numpy(W.kmers_host.numpy()).cuda()
+    if keys is None or args.no_replay:
+        return None
+    nq = keys.numel()
+    res = {"what": "ph_gpu_gather_replay_u64: key stream (8 B) + one pilot gather per key at "
+                   "the true bucket address, no slot arithmetic / remap / output",
+           "direct_order_ms": round(time_ms(lambda: idx.gather_replay(keys)), 4)}
+    pb = int(info.pilot_bytes)
+    if pb > (64 << 20):
+        G = max(2, -(-pb // (32 << 20)))  # ph_abi.cu partition_groups (32 MiB slices)
+        C_ = 0x517CC1B727220A95  # kMixConstant (hash.hpp:13), < 2^63
+        seed = int(info.seed)
+        seed = seed - (1 << 64) if seed >= (1 << 63) else seed
+        h = (keys ^ seed) * C_  # wrapping int64 multiply = hash_int (hash.hpp:27)
+        g = (((h >> 32) & 0xFFFFFFFF) * G) >> 32
+        del h
+        order = torch.sort(g, stable=True).indices
+        del g
+        grouped = keys[order]
+        del order
+        res["grouped_order_ms"] = round(time_ms(lambda: idx.gather_replay(grouped)), 4)
+        res["groups"] = G
+        del grouped
+    res["gathers_per_step"] = nq
+    return res
+
+
+def run_secondaries(args):
+    """Configs 4 (strings) and 5 (k-mers) in their own processes (same steps / warm-up, full
+    gate, CPU matrix), so the driver's default run carries their numbers next to config 3."""
+    import subprocess
+    out = {}
+    for c in (4, 5):
+        if c == args.config:
+            continue
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", str(c), "--steps",
+               str(args.steps), "--warmup", str(args.warmup), "--verify", args.verify,
+               "--cpu-sample", str(args.cpu_sample), "--no-secondary"]
+        t = time.time()
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        sys.stderr.write(p.stderr[-4000:])
+        lines = [x for x in p.stdout.splitlines() if x.startswith("{")]
+        if p.returncode == 0 and lines:
+            d = json.loads(lines[-1])
+            d["driver_note"] = f"run by bench.py as a subprocess in {time.time() - t:.0f} s"
+            out[f"config{c}"] = d
+        else:
+            out[f"config{c}"] = {"error": f"rc={p.returncode}", "stderr": p.stderr[-1500:]}
+    return out
+
+
+CPU_MODES = (("loop", 0), ("stream", 32), ("batched", 64))  # ptrhash.cpp:160-174 run_mode
+
+
+def time_best(fn, reps=3):
+    """One warm-up, then the best of `reps` (proj/tools/ptrhash.cpp:212-223)."""
     fn()
     best = 1e30
-    for _ in range(3):
+    for _ in range(reps):
         t = time.perf_counter()
         fn()
         best = min(best, time.perf_counter() - t)
+    return best
+
+
+def cpu_baseline(W, args):
+    """The reference's own CPU query path on this box's host cores (SURVEY
+    §8d): T = 1 and T = all hardware threads x index_loop / index_stream(32) /
+    index_batched(64) x minimal / non-minimal, contiguous slices per thread as the CLI bench
+    does (ptrhash.cpp:486-512), one warm-up and the best of 3 (:212-223), each cell on a
+    bounded sample of this config's query stream. `value` is the T = all, index_stream(32),
+    minimal cell (the reference's recommended bulk query)."""
+    from oracle.bindings import Ref
+    ri = Ref().load(W.ptrh)
+    T = os.cpu_count() or 1
+    S_all = min(W.nq, args.cpu_sample if W.cfg["kind"] != "str" else args.cpu_sample // 4)
+    S_one = min(S_all, max(args.cpu_sample // 50, 1))
+    run, what, close = W.cpu_runner(ri, S_all)
+    cells = []
+    t0 = time.time()
+    for threads, S in ((1, S_one), (T, S_all)):
+        for mode, width in CPU_MODES:
+            for minimal in (True, False):
+                sec = time_best(lambda: run(S, minimal, mode, width, threads))
+                cells.append({"threads": threads, "mode": mode if not width else f"{mode}:{width}",
+                              "minimal": minimal, "ns_per_key": round(sec / S * 1e9, 3),
+                              "gkeys_s": round(S / sec / 1e9, 4), "sample": S})
+    close()
     ri.close()
-    return {"value": round(S / best / 1e9, 4), "unit": "Gkeys/s",
-            "ns_per_key": round(best / S * 1e9, 3), "cores": os.cpu_count() or 1,
-            "kind": "reference", "sample": desc + ", best of 3 after 1 warm-up"}
+    head = next(c for c in cells if c["threads"] == T and c["mode"] == "stream:32" and c["minimal"])
+    log(f"[cpu] reference matrix ({len(cells)} cells) in {time.time() - t0:.1f}s")
+    return {"value": head["gkeys_s"], "unit": "Gkeys/s", "ns_per_key": head["ns_per_key"],
+            "cores": T, "kind": "reference", "cpu_model": cpu_model(),
+            "sample": (f"first {S_all} {what}; reference PtrHashIndex::index_stream(lookahead "
+                       f"32), minimal, {T} threads, contiguous slices, best of 3 after 1 "
+                       f"warm-up (the full matrix is in `matrix`; T=1 cells use the first "
+                       f"{S_one})"),
+            "matrix": cells}
 
 
 # ---------------------------------------------------------------------------
@@ -735,11 +921,14 @@ def run_reference(args, cfg):
         data, offs = port.gen_strings(0, n, n, STR_SEED)
         ptrh = ref.build_bytes(data, offs, ref_params(ref), lean=True)
         del data, offs
+        from oracle.bindings import RefStrings
+        S = min(n, args.cpu_sample // 4)  # as our arm's cpu_baseline (std::string keys)
         qd, qo = port.gen_strings(0, S, n, STR_SEED, PERM_SEED)
         ri = ref.load(ptrh)
         out = np.empty(S, dtype=np.uint64)
-        step = lambda: ri.query_bytes(qd, qo, True, "single", threads=T, out=out)  # noqa: E731
-        what = "index(string_view) over the concatenated buffer"
+        rs = RefStrings(ref, qd, qo)  # std::string keys made before timing
+        step = lambda: rs.query(ri, True, "stream", 32, threads=T, out=out)  # noqa: E731
+        what = "index_stream(lookahead 32) over std::string keys"
     else:
         k = cfg["k"]
         n_bases = cfg["n"] + k - 1
@@ -773,9 +962,12 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "n": cfg["n"], "params": "preset default, lambda=3.0"},
+        "config": config_dict(cfg, ptrh, int(os.environ.get("WORLD_SIZE", "1"))),
+        "reference_sample": (f"each step times the first {S} of the {cfg['nq']} queries of the "
+                             f"same stream; Gkeys/s is per query, so it compares with our "
+                             f"arm's whole-stream steps"),
         "cpu_baseline": {"value": round(value, 5), "unit": "Gkeys/s", "cores": T,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 5), "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -791,6 +983,9 @@ def main():
     ap.add_argument("--verify", default="full", choices=["full", "sample", "none"])
     ap.add_argument("--cpu-sample", type=int, default=100_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--no-secondary", dest="secondary_configs", action="store_false",
+                    help="do not run configs 4 and 5 after the main config (N=1)")
     ap.add_argument("--layout", default="", choices=["", "file", "hot", "default"],
                     help="override the config's pilot layout (file: partitioned path when large; "
                          "hot: hot-first layout + persisting window, the direct kernel)")
@@ -799,6 +994,7 @@ def main():
         log("note: warmup raised to 3 (timing rules)")
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
+    cfg["nq"] = cfg["n"]  # queries per step: every config queries n keys (k-mers: n windows)
     if args.layout:
         cfg["layout"] = args.layout
     if args.impl == "reference":

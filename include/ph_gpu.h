@@ -73,6 +73,11 @@ int ph_gpu_index_destroy(ph_gpu_index* index);
  * largest batch in the index's memory pool between calls) to the device. Memory still in use
  * by queries in flight is kept; later queries allocate again. */
 int ph_gpu_index_trim(const ph_gpu_index* index);
+/* Ceiling on the per-call scratch an index keeps cached between calls (the pool's release
+ * threshold; default: a quarter of the device's memory). Scratch above it returns to the
+ * device at the caller's next synchronisation, so a later large call maps it again (~1 ms
+ * per GB). 0 keeps nothing. */
+int ph_gpu_index_set_scratch_limit(ph_gpu_index* index, uint64_t bytes);
 int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out);
 const char* ph_gpu_last_error(void);
 
@@ -146,6 +151,13 @@ int ph_gpu_bucket_sizes(const ph_gpu_index* index, const uint64_t* d_keys, size_
  * outputs >= n and the repeated outputs among d_out[0..count) (u32 or u64). */
 int ph_gpu_verify_bijection(const void* d_out, size_t count, int out_width, uint64_t n,
                             int device, uint64_t* out_of_range, uint64_t* duplicates);
+
+/* Measurement (bench.py's replay bound): the query path's pilot reads alone at
+ * the index's true bucket addresses, in the order of d_keys (u64 keys, async on stream):
+ * the keys are streamed and each key's pilot byte is gathered as the query kernels do, with
+ * no slot arithmetic, remap or output. */
+int ph_gpu_gather_replay_u64(const ph_gpu_index* index, const uint64_t* d_keys, size_t n,
+                             ph_gpu_stream_t stream);
 
 /* ---- introspection ---- */
 /* Number of query-kernel launches this process made through this library. */

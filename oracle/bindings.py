@@ -72,6 +72,11 @@ class Ref:
                                     C.c_size_t, C.c_uint]
         L.ref_query_bytes.argtypes = [C.c_void_p, u8p, u64p, C.c_size_t, u64p, C.c_int,
                                       C.c_int, C.c_size_t, C.c_uint]
+        L.ref_strings_new.argtypes = [u8p, u64p, C.c_size_t]
+        L.ref_strings_new.restype = C.c_void_p
+        L.ref_strings_free.argtypes = [C.c_void_p]
+        L.ref_query_strings.argtypes = [C.c_void_p, C.c_void_p, u64p, C.c_int, C.c_int,
+                                        C.c_size_t, C.c_uint]
         L.ref_preset.argtypes = [C.c_char_p, C.POINTER(RefParams)]
         L.ref_compute_shape.argtypes = [C.c_uint64, C.POINTER(RefParams), u64p, u64p, u64p]
         for name in ("ref_mix_constant_inverse",):
@@ -265,6 +270,39 @@ class RefIndex:
         if rc:
             raise RuntimeError(self.ref.err())
         return out
+
+
+class RefStrings:
+    """std::string keys materialised once (ref_strings_new), for timing the reference's
+    span<const std::string> bulk queries without the string construction."""
+
+    def __init__(self, ref: Ref, data, offsets):
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        self.ref, self.n = ref, offsets.size - 1
+        self.h = ref.L.ref_strings_new(_ptr(data, u8p), _ptr(offsets), self.n)
+        if not self.h:
+            raise MemoryError(ref.err())
+
+    def query(self, ri: "RefIndex", minimal=True, mode="stream", width=32, threads=1, out=None):
+        if out is None:
+            out = np.empty(self.n, dtype=np.uint64)
+        rc = self.ref.L.ref_query_strings(ri.h, self.h, _ptr(out), int(minimal),
+                                          RefIndex.MODES[mode], width, threads)
+        if rc:
+            raise RuntimeError(self.ref.err())
+        return out
+
+    def close(self):
+        if self.h:
+            self.ref.L.ref_strings_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class PhoIndex(C.Structure):

@@ -283,6 +283,33 @@ int ref_query_bytes(const void* h, const uint8_t* data, const uint64_t* offsets,
     });
 }
 
+// Pre-materialised std::string keys (so a timed index_loop / index_batched / index_stream
+// over span<const std::string> excludes building the strings; bench.py's CPU matrix).
+void* ref_strings_new(const uint8_t* data, const uint64_t* offsets, size_t n) {
+    try {
+        return new std::vector<std::string>(to_strings(data, offsets, 0, n));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void ref_strings_free(void* s) { delete static_cast<std::vector<std::string>*>(s); }
+// mode: 0 = index_loop, 1 = index_batched(width), 2 = index_stream(width), over T slices
+int ref_query_strings(const void* h, const void* strs, uint64_t* out, int minimal, int mode,
+                      size_t width, unsigned threads) {
+    return guarded([&] {
+        const auto* idx = static_cast<const PtrHashIndex*>(h);
+        const auto& v = *static_cast<const std::vector<std::string>*>(strs);
+        run_slices(v.size(), threads, [&](size_t b, size_t e) {
+            std::span<const std::string> sp(v.data() + b, e - b);
+            if (mode == 0) idx->index_loop(sp, out + b, minimal != 0);
+            else if (mode == 1) idx->index_batched(sp, width, out + b, minimal != 0);
+            else idx->index_stream(sp, width, out + b, minimal != 0);
+        });
+        return 0;
+    });
+}
+
 // ---- primitives for known-answer tests ----
 uint64_t ref_mix_constant_inverse() { return mix_constant_inverse(); }
 uint64_t ref_hash_int(uint64_t k, uint64_t seed) { return hash_int(k, seed); }

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -122,7 +123,15 @@ struct ph_gpu_index {
     // host-path pipelines (streams + staging buffers), reused across calls
     mutable std::mutex pl_mu;
     mutable std::vector<Pipeline*> pl_cache;
-    void (*pl_free)(ph_gpu_index*) = nullptr;  // frees pl_cache (defined with Pipeline)
+    void (*pl_free)(ph_gpu_index*) = nullptr;  // frees pl_cache (set at create)
+    // single-key queries (index() / index_no_remap()): one block of mapped pinned host
+    // memory (key, offsets, output, key bytes) the kernel reads and writes in place, and
+    // one stream, reused under single_mu: no allocation or copy call per query
+    mutable std::mutex single_mu;
+    mutable uint8_t* single_h = nullptr;
+    mutable uint8_t* single_d = nullptr;  // device alias of single_h
+    mutable size_t single_cap = 0;
+    mutable cudaStream_t single_s = nullptr;
 };
 
 namespace {
@@ -225,56 +234,137 @@ int upload(const void* src, size_t bytes, void** dst) {
     return PH_OK;
 }
 
-// Uploads the file-order pilots `file` (P*B bytes) in the hot-first layout for
-// `hot_bytes` and sets the persisting-L2 window over the hot region.
+// Single-key scratch (caller holds single_mu; the index's device is current).
+constexpr size_t kSingleHeader = 64;  // [0] key / offsets[2] at 0..15, output at 16
+int ensure_single(const ph_gpu_index* ix, size_t key_bytes) {
+    const size_t need = kSingleHeader + ((key_bytes + 15) & ~size_t{15}) + 16;
+    if (!ix->single_s) {
+        cudaError_t e = cudaStreamCreateWithFlags(&ix->single_s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "single-key stream");
+    }
+    if (ix->single_cap >= need) return PH_OK;
+    if (ix->single_h) cudaFreeHost(ix->single_h);
+    ix->single_h = ix->single_d = nullptr;
+    ix->single_cap = 0;
+    size_t cap = need < 4096 ? 4096 : need * 2;
+    void* h = nullptr;
+    cudaError_t e = cudaHostAlloc(&h, cap, cudaHostAllocMapped);
+    if (e != cudaSuccess) return fail(PH_E_NOMEM, "single-key scratch (mapped pinned memory)");
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, h, 0);
+    if (e != cudaSuccess) {
+        cudaFreeHost(h);
+        return cuda_fail(e, "cudaHostGetDevicePointer");
+    }
+    std::memset(h, 0, cap);
+    ix->single_h = static_cast<uint8_t*>(h);
+    ix->single_d = static_cast<uint8_t*>(d);
+    ix->single_cap = cap;
+    return PH_OK;
+}
+void free_single(ph_gpu_index* ix) {
+    if (ix->single_s) cudaStreamSynchronize(ix->single_s);
+    if (ix->single_h) cudaFreeHost(ix->single_h);
+    if (ix->single_s) cudaStreamDestroy(ix->single_s);
+    ix->single_h = ix->single_d = nullptr;
+    ix->single_s = nullptr;
+}
+
+// The device-wide persisting-L2 set-aside is shared by every index on a device: each live
+// index registers the set-aside its window wants (0: none), and the device limit is the
+// largest wanted by any of them, so creating or re-laying out one index never cancels
+// another's window. (Consequence, documented in ph_gpu.h: while an index with a window is
+// live, the partitioned path of a DRAM-sized index runs with that set-aside in place.)
+std::mutex g_l2_mu;
+std::map<int, std::map<const ph_gpu_index*, size_t>> g_l2_wants;
+
+// Sets this device's limit to the largest registered want; returns the limit now in force.
+size_t l2_apply_limit_locked(int device) {
+    size_t want = 0;
+    for (const auto& kv : g_l2_wants[device]) want = kv.second > want ? kv.second : want;
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur != want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
+        cudaGetLastError();
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    return cur;
+}
+
+void l2_unregister(const ph_gpu_index* ix) {
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    auto& m = g_l2_wants[ix->device];
+    if (m.erase(ix)) l2_apply_limit_locked(ix->device);
+}
+
+// Uploads the file-order pilots `file` (P*B bytes) in the hot-first layout for `hot_bytes`
+// and sets the persisting-L2 window over the hot region. The new device buffer is built
+// first; only when it is complete does it replace the index's pilots and layout fields, so
+// a failure leaves the index as it was.
 int apply_pilot_layout(ph_gpu_index* ix, const uint8_t* file, uint64_t hot_bytes, int flags) {
     const uint64_t P = ix->info.parts, B = ix->info.buckets_per_part;
     const uint64_t total = P * B;
     uint64_t H = B;  // hot_bytes == 0 or everything fits: the file's own order
     if (hot_bytes && total > hot_bytes && P > 0) H = hot_bytes / P < B ? hot_bytes / P : B;
-    phg::DevIndex& d = ix->dev;
-    int rc = upload(file, total, &ix->d_pilots);  // file order
-    if (rc) return rc;
+    void* buf = nullptr;
+    int rc = upload(file, total, &buf);  // file order
+    if (rc) {
+        cudaFree(buf);
+        return rc;
+    }
     if (H != B) {  // permute to the hot-first layout on the device (k_relayout)
         void* lay = nullptr;
         cudaError_t e = cudaMalloc(&lay, total);
-        if (e != cudaSuccess) return fail(PH_E_NOMEM, "cudaMalloc(pilot layout)");
-        e = phg::launch_relayout(static_cast<const uint8_t*>(ix->d_pilots),
-                                 static_cast<uint8_t*>(lay), P, B, H, nullptr);
+        if (e != cudaSuccess) {
+            cudaFree(buf);
+            return fail(PH_E_NOMEM, "cudaMalloc(pilot layout)");
+        }
+        e = phg::launch_relayout(static_cast<const uint8_t*>(buf), static_cast<uint8_t*>(lay), P,
+                                 B, H, nullptr);
         if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
-        cudaFree(ix->d_pilots);
-        ix->d_pilots = lay;
-        if (e != cudaSuccess) return cuda_fail(e, "pilot relayout");
+        cudaFree(buf);
+        if (e != cudaSuccess) {
+            cudaFree(lay);
+            return cuda_fail(e, "pilot relayout");
+        }
+        buf = lay;
     }
-    d.pilots = static_cast<const uint8_t*>(ix->d_pilots);
+    // the window this layout wants (0: none)
+    uint64_t win = 0;
+    size_t want = 0;
+    if (!(flags & kL2NoWindow) && hot_bytes) {
+        int max_window = 0, max_persist = 0;
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ix->device);
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ix->device);
+        if (max_window > 0 && max_persist > 0 && P * H > 0) {
+            win = P * H < (uint64_t)max_window ? P * H : (uint64_t)max_window;
+            want = win < (uint64_t)max_persist ? win : (uint64_t)max_persist;
+        }
+    }
+    // swap in the new layout
+    phg::DevIndex& d = ix->dev;
+    if (ix->d_pilots) {
+        cudaDeviceSynchronize();  // (set_l2_policy: no query may still read the old buffer)
+        cudaFree(ix->d_pilots);
+    }
+    ix->d_pilots = buf;
+    d.pilots = static_cast<const uint8_t*>(buf);
     d.hot_b = H;
     d.cold_b = B - H;
     d.hot_total = P * H;
     d.cold_evict_first = (flags & kL2ColdEvictFirst) ? 1 : 0;
     d.window_bytes = 0;
     d.window_hit_ratio = 0.f;
-    // Lines left persisting by earlier windowed launches would otherwise keep their share
-    // of the L2 (the partitioned path's pass B needs all of it).
-    cudaCtxResetPersistingL2Cache();
-    if ((flags & kL2NoWindow) || !hot_bytes) {
-        // No window: also release the device-wide persisting set-aside, which otherwise
-        // shrinks the L2 left to normal accesses (measured: partitioned pass B 2x slower).
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0) != cudaSuccess) cudaGetLastError();
-        return PH_OK;
-    }
-    int max_window = 0, max_persist = 0;
-    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ix->device);
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ix->device);
-    if (max_window > 0 && max_persist > 0 && d.hot_total > 0) {
-        const uint64_t win = d.hot_total < (uint64_t)max_window ? d.hot_total : (uint64_t)max_window;
-        size_t cur = 0;
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        const size_t want = win < (uint64_t)max_persist ? win : (uint64_t)max_persist;
-        if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
-            cudaGetLastError();  // persisting L2 unavailable: run without the window
-            return PH_OK;
-        }
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    auto& wants = g_l2_wants[ix->device];
+    wants[ix] = want;
+    // Lines left persisting by earlier windowed launches would keep their share of the L2
+    // (the partitioned path's pass B needs all of it): reset them only when no live index
+    // on this device has a window that relies on them.
+    bool other_window = false;
+    for (const auto& kv : wants) other_window |= kv.first != ix && kv.second > 0;
+    if (!other_window) cudaCtxResetPersistingL2Cache();
+    const size_t cur = l2_apply_limit_locked(ix->device);
+    if (win && cur > 0) {
         d.window_bytes = win;
         d.window_hit_ratio = cur >= win ? 1.f : static_cast<float>(cur) / static_cast<float>(win);
     }
@@ -284,6 +374,8 @@ int apply_pilot_layout(ph_gpu_index* ix, const uint8_t* file, uint64_t hot_bytes
 void release(ph_gpu_index* ix) {
     if (!ix) return;
     DeviceGuard g(ix->device);
+    l2_unregister(ix);
+    free_single(ix);
     if (ix->pl_free) ix->pl_free(ix);
     cudaFree(ix->d_pilots);
     cudaFree(ix->d_remap);
@@ -408,6 +500,10 @@ bool is_pinned_host(const void* p) {
 
 extern "C" {
 
+namespace {
+void free_pipelines(ph_gpu_index* ix);  // (with the host-path pipelines below)
+}
+
 const char* ph_gpu_last_error(void) { return g_err.c_str(); }
 uint64_t ph_gpu_launch_count(void) { return phg::launch_count(); }
 int ph_gpu_set_pass_timing(int on) {
@@ -459,6 +555,7 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
 
     auto* ix = new ph_gpu_index();
     ix->device = device;
+    ix->pl_free = free_pipelines;
     cudaDeviceGetAttribute(&ix->sms, cudaDevAttrMultiProcessorCount, device);
     ph_gpu_info& I = ix->info;
     I.n = p.n;
@@ -554,7 +651,15 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
         props.location.type = cudaMemLocationTypeDevice;
         props.location.id = device;
         if (cudaMemPoolCreate(&ix->pool, &props) == cudaSuccess) {
-            uint64_t keep = ~uint64_t{0};
+            // Freed per-call scratch stays mapped for the next call up to a ceiling of a
+            // quarter of the device's memory (a 1e9-key partitioned call takes ~29 GB, and
+            // re-mapping it costs ~27 ms per call: measured 37.4 vs 10.2 ms per step with a
+            // 2 GiB ceiling); beyond the ceiling it goes back to the device at the caller's
+            // next synchronisation. ph_gpu_index_set_scratch_limit changes the ceiling,
+            // ph_gpu_index_trim releases everything not in use.
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            uint64_t keep = total_b / 4;
             cudaMemPoolSetAttribute(ix->pool, cudaMemPoolAttrReleaseThreshold, &keep);
         } else {
             cudaGetLastError();
@@ -579,6 +684,16 @@ int ph_gpu_index_trim(const ph_gpu_index* index) {
     return e == cudaSuccess ? PH_OK : cuda_fail(e, "cudaMemPoolTrimTo");
 }
 
+int ph_gpu_index_set_scratch_limit(ph_gpu_index* index, uint64_t bytes) {
+    if (!index) return fail(PH_E_INVALID, "null index");
+    if (!index->pool) return PH_OK;
+    DeviceGuard g(index->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    const cudaError_t e =
+        cudaMemPoolSetAttribute(index->pool, cudaMemPoolAttrReleaseThreshold, &bytes);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "cudaMemPoolSetAttribute");
+}
+
 int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flags) {
     if (!index) return fail(PH_E_INVALID, "null index");
     DeviceGuard g(index->device);
@@ -593,9 +708,7 @@ int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flag
         std::memcpy(file.data() + part * B, cur.data() + part * H, H);
         std::memcpy(file.data() + part * B + H, cur.data() + P * H + part * (B - H), B - H);
     }
-    cudaFree(index->d_pilots);
-    index->d_pilots = nullptr;
-    return apply_pilot_layout(index, file.data(), hot_bytes, flags);
+    return apply_pilot_layout(index, file.data(), hot_bytes, flags);  // swaps only on success
 }
 
 int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out) {
@@ -613,6 +726,7 @@ int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, v
     if (n == 0) return PH_OK;
     if (!d_keys || !d_out) return fail(PH_E_INVALID, "null key or output pointer");
     DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     if (const uint32_t G = partition_groups(ix, n, out_width)) {
         const cudaError_t pe = run_partitioned(ix, d_keys, 0, 0, 0, d_out, out_width, n, minimal,
                                                G, static_cast<cudaStream_t>(stream));
@@ -636,6 +750,7 @@ int ph_gpu_query_bytes(const ph_gpu_index* ix, const uint8_t* d_bytes, const uin
     if (n == 0) return PH_OK;
     if (!d_bytes || !d_offsets || !d_out) return fail(PH_E_INVALID, "null pointer argument");
     DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     cudaError_t e = phg::launch_query_bytes(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_bytes,
                                             d_offsets, 0, d_out, out_width, n, minimal,
                                             static_cast<cudaStream_t>(stream), ix->sms);
@@ -739,7 +854,6 @@ int lease_pipeline(const ph_gpu_index* ix, size_t in_bytes, size_t off_bytes, si
             }
         }
     }
-    const_cast<ph_gpu_index*>(ix)->pl_free = free_pipelines;
     auto* p = new Pipeline();
     if (int rc = alloc_pipeline(*p, in_bytes, off_bytes, out_bytes, bounce)) {
         delete p;
@@ -778,10 +892,14 @@ int ph_gpu_index_stream_u64(const ph_gpu_index* ix, const uint64_t* h_keys, size
     if (!h_keys || !h_out) return fail(PH_E_INVALID, "null key or output pointer");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-    if (is_device_ptr(h_keys) || is_device_ptr(h_out)) {  // device spans: no staging
-        if (int rc = ph_gpu_query_u64(ix, h_keys, n, h_out, out_width, minimal, nullptr)) return rc;
-        PH_CUDA(cudaStreamSynchronize(nullptr));
-        return PH_OK;
+    {
+        const bool dk = is_device_ptr(h_keys), dout = is_device_ptr(h_out);
+        if (dk != dout) return fail(PH_E_INVALID, "keys and out must both be host or both device memory");
+        if (dk) {  // device spans: no staging
+            if (int rc = ph_gpu_query_u64(ix, h_keys, n, h_out, out_width, minimal, nullptr)) return rc;
+            PH_CUDA(cudaStreamSynchronize(nullptr));
+            return PH_OK;
+        }
     }
     const size_t C = chunk_keys(n);
     const bool bounce = !(is_pinned_host(h_keys) && is_pinned_host(h_out));
@@ -843,6 +961,19 @@ int ph_gpu_index_stream_bytes(const ph_gpu_index* ix, const uint8_t* h_bytes,
     if (!h_bytes || !h_offsets || !h_out) return fail(PH_E_INVALID, "null pointer argument");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    {
+        const bool db = is_device_ptr(h_bytes), doff = is_device_ptr(h_offsets),
+                   dout = is_device_ptr(h_out);
+        if (db != doff || db != dout)
+            return fail(PH_E_INVALID, "bytes, offsets and out must all be host or all device memory");
+        if (db) {  // device spans: no staging
+            if (int rc = ph_gpu_query_bytes(ix, h_bytes, h_offsets, n, h_out, out_width, minimal,
+                                            nullptr))
+                return rc;
+            PH_CUDA(cudaStreamSynchronize(nullptr));
+            return PH_OK;
+        }
+    }
     const size_t C = chunk_keys(n);
     size_t max_bytes = 0;
     for (size_t off = 0; off < n; off += C) {
@@ -913,6 +1044,7 @@ int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n
     if (n_bases < (uint64_t)k) return PH_OK;
     if (!d_seq || !d_out) return fail(PH_E_INVALID, "null sequence or output pointer");
     DeviceGuard g(ix->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     const uint64_t nwin = n_bases - (uint64_t)k + 1;
     if (const uint32_t G = partition_groups(ix, nwin, out_width)) {
         const cudaError_t pe = run_partitioned(ix, d_seq, 1, (n_bases + 31) / 32, (uint32_t)(2 * k),
@@ -939,6 +1071,16 @@ int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uin
     if (!h_seq || !h_out) return fail(PH_E_INVALID, "null sequence or output pointer");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    {
+        const bool ds = is_device_ptr(h_seq), dout = is_device_ptr(h_out);
+        if (ds != dout) return fail(PH_E_INVALID, "seq and out must both be host or both device memory");
+        if (ds) {  // device spans: no staging
+            if (int rc = ph_gpu_query_kmers(ix, h_seq, n_bases, k, h_out, out_width, minimal, nullptr))
+                return rc;
+            PH_CUDA(cudaStreamSynchronize(nullptr));
+            return PH_OK;
+        }
+    }
     const uint64_t n = n_bases - (uint64_t)k + 1;  // windows
     const uint64_t nwords_total = (n_bases + 31) / 32;
     const size_t C = chunk_keys(n) & ~size_t{31} ? chunk_keys(n) & ~size_t{31} : 32;  // windows
@@ -995,21 +1137,26 @@ int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uin
     return PH_OK;
 }
 
-// Single-key queries: one small device scratch block, synchronous.
+// Single-key queries (index.hpp:60-64), synchronous: the key is written into the index's
+// mapped pinned block, one kernel launch reads it and writes the answer back in place, and
+// the call waits on the index's single-key stream. Many host threads may call at once; they
+// take turns on the block.
 int ph_gpu_index_u64(const ph_gpu_index* ix, uint64_t key, int minimal, uint64_t* out) {
     if (!ix || !out) return fail(PH_E_INVALID, "null argument");
     if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-    uint64_t* d = nullptr;
-    PH_CUDA(cudaMalloc(&d, 16));
-    cudaError_t e = cudaMemcpy(d, &key, 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2, d, d + 1, 8, 1,
-                                  minimal, nullptr, ix->sms);
-    if (e == cudaSuccess) e = cudaMemcpy(out, d + 1, 8, cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    return e == cudaSuccess ? PH_OK : cuda_fail(e, "index_u64");
+    std::lock_guard<std::mutex> lk(ix->single_mu);
+    if (int rc = ensure_single(ix, 0)) return rc;
+    auto* h = reinterpret_cast<volatile uint64_t*>(ix->single_h);
+    auto* d = reinterpret_cast<uint64_t*>(ix->single_d);
+    h[0] = key;
+    cudaError_t e = phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2, d, d + 2, 8,
+                                          1, minimal, ix->single_s, ix->sms);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ix->single_s);
+    if (e != cudaSuccess) return cuda_fail(e, "index_u64");
+    *out = h[2];
+    return PH_OK;
 }
 
 int ph_gpu_index_bytes(const ph_gpu_index* ix, const uint8_t* key, size_t len, int minimal,
@@ -1018,20 +1165,20 @@ int ph_gpu_index_bytes(const ph_gpu_index* ix, const uint8_t* key, size_t len, i
     if (ix->info.key_kind != 1) return fail(PH_E_KEYKIND, "string query on a u64-key index");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-    const size_t words = 3 + (len + 7) / 8;  // offsets[2], out, bytes
-    uint64_t* d = nullptr;
-    PH_CUDA(cudaMalloc(&d, words * 8));
-    std::vector<uint64_t> h(words, 0);
+    std::lock_guard<std::mutex> lk(ix->single_mu);
+    if (int rc = ensure_single(ix, len)) return rc;
+    auto* h = reinterpret_cast<volatile uint64_t*>(ix->single_h);
+    auto* d = reinterpret_cast<uint64_t*>(ix->single_d);
+    h[0] = 0;  // offsets {0, len}; the bytes follow the header
     h[1] = len;
-    if (len) std::memcpy(h.data() + 3, key, len);
-    cudaError_t e = cudaMemcpy(d, h.data(), words * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = phg::launch_query_bytes(ix->dev, ix->info.bucket_fn, ix->info.pow2,
-                                    reinterpret_cast<const uint8_t*>(d + 3), d, 0, d + 2, 8, 1,
-                                    minimal, nullptr, ix->sms);
-    if (e == cudaSuccess) e = cudaMemcpy(out, d + 2, 8, cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    return e == cudaSuccess ? PH_OK : cuda_fail(e, "index_bytes");
+    if (len) std::memcpy(ix->single_h + kSingleHeader, key, len);
+    cudaError_t e = phg::launch_query_bytes(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                            ix->single_d + kSingleHeader, d, 0, d + 2, 8, 1,
+                                            minimal, ix->single_s, ix->sms);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ix->single_s);
+    if (e != cudaSuccess) return cuda_fail(e, "index_bytes");
+    *out = h[2];
+    return PH_OK;
 }
 
 // load_index (serde.cpp:251-260) for the GPU: the PTRH file is mmap'ed, pinned in place
@@ -1115,6 +1262,23 @@ int ph_gpu_bucket_sizes(const ph_gpu_index* index, const uint64_t* d_keys, size_
     if (e != cudaSuccess) return cuda_fail(e, "bucket_sizes");
     *len = l;
     return PH_OK;
+}
+
+int ph_gpu_gather_replay_u64(const ph_gpu_index* index, const uint64_t* d_keys, size_t n,
+                             ph_gpu_stream_t stream) {
+    if (!index || (!d_keys && n)) return fail(PH_E_INVALID, "null argument");
+    if (index->info.key_kind != 0) return fail(PH_E_KEYKIND, "index was built over byte-string keys");
+    DeviceGuard g(index->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* sink = nullptr;
+    cudaError_t e = index->pool ? cudaMallocFromPoolAsync(&sink, 256, index->pool, s)
+                                : cudaMallocAsync(&sink, 256, s);
+    if (e != cudaSuccess) return cuda_fail(e, "gather_replay scratch");
+    e = phg::launch_gather_replay(index->dev, index->info.bucket_fn, d_keys, n,
+                                  static_cast<uint32_t*>(sink), s, index->sms);
+    cudaFreeAsync(sink, s);
+    return e == cudaSuccess ? PH_OK : cuda_fail(e, "gather_replay");
 }
 
 }  // extern "C"

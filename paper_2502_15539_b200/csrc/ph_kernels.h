@@ -89,6 +89,10 @@ cudaError_t bucket_size_hist(const DevIndex& ix, int gamma_kind, const uint64_t*
                              uint64_t* hist_out, uint64_t cap, uint64_t* len_out, cudaStream_t s,
                              int sms);
 
+// Gather-only replay of the pilot reads at the true bucket addresses (bench.py roofline).
+cudaError_t launch_gather_replay(const DevIndex& ix, int gamma_kind, const uint64_t* keys,
+                                 uint64_t n, uint32_t* sink, cudaStream_t s, int sms);
+
 cudaError_t launch_relayout(const uint8_t* src, uint8_t* dst, uint64_t P, uint64_t B, uint64_t H,
                             cudaStream_t s);
 cudaError_t launch_verify(const void* out, int out_width, uint64_t count, uint64_t n,

@@ -349,6 +349,56 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
 }
 
 // ---------------------------------------------------------------------------
+// Gather-only replay (measurement: bench.py's replay bound). The pilot reads of
+// the query path at the index's true bucket addresses, in the order of `keys`, with the same
+// key stream (8 B/key, evict_first) and the same pilot loads (evict_last) as pass B, and
+// none of the slot arithmetic, remap or output: what those gathers alone cost. Over keys in
+// query order it bounds the direct kernel; over keys sorted by partition group (pass B's
+// order) it bounds pass B.
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(256, 4) k_gather_replay(const DevIndex ix,
+                                                         const uint64_t* __restrict__ keys,
+                                                         uint64_t n, uint32_t* __restrict__ sink) {
+    constexpr int KPT = 8;
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+    const uint32_t P32 = (uint32_t)ix.P, B32 = (uint32_t)ix.B;
+    uint32_t acc = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * KPT;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * KPT; base < n; base += stride) {
+        uint32_t pilot[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const uint64_t i = base + (uint64_t)j * blockDim.x + threadIdx.x;
+            const uint64_t h = kC * ((i < n ? ld_stream_u64(keys + i, pol_stream) : 0) ^ ix.seed);
+            uint64_t x;
+            const uint32_t part = (uint32_t)mul32x64(P32, h, x);
+            const uint32_t bucket = bucket_of<G>(x, B32, ix.opt_table);
+            pilot[j] = ld_gather_u8(ix.pilots + ((uint64_t)part * B32 + bucket), pol_keep);
+        }
+#pragma unroll
+        for (int j = 0; j < KPT; j++) acc += pilot[j];
+    }
+    if (acc == 0xffffffffu) sink[0] = acc;  // (never: keeps the loads)
+}
+
+cudaError_t launch_gather_replay(const DevIndex& ix, int gamma_kind, const uint64_t* keys,
+                                 uint64_t n, uint32_t* sink, cudaStream_t s, int sms) {
+    if (n == 0) return cudaSuccess;
+    const int grid = sms * 4;
+    switch (gamma_kind) {
+        case 0: k_gather_replay<0><<<grid, 256, 0, s>>>(ix, keys, n, sink); break;
+        case 1: k_gather_replay<1><<<grid, 256, 0, s>>>(ix, keys, n, sink); break;
+        case 2: k_gather_replay<2><<<grid, 256, 0, s>>>(ix, keys, n, sink); break;
+        case 3: k_gather_replay<3><<<grid, 256, 0, s>>>(ix, keys, n, sink); break;
+        case 4: k_gather_replay<4><<<grid, 256, 0, s>>>(ix, keys, n, sink); break;
+        default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // index upload helper and the bijection verifier
 // ---------------------------------------------------------------------------
 // File-order pilots (P*B) -> hot-first layout, one part per block iteration.

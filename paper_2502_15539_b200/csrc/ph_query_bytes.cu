@@ -42,36 +42,23 @@ __constant__ uint8_t c_sbox[256] = {
 
 // The MixColumns∘SubBytes tables T0[x] = (2·S[x], S[x], S[x], 3·S[x]) (rows 0..3, LE) and
 // its rotations T1..T3 (by 8/16/24 bits), each held in shared memory 32 times, interleaved
-// so that entry x of copy `lane` sits at byte offset x*128 + lane*4: every lane reads its
-// own copy, i.e. its own bank, so the 16 lookups of an AES round are conflict-free whatever
-// the state bytes are, and a column is four lookups XORed with no rotates. S[x] is byte 1
-// of T0[x] (for AESENCLAST). PH_STR_T1 = 0 keeps T0 only (rotates in the round), 1 keeps
-// T0 and T1. With 4 tables (128 KiB) one 1024-thread CTA per SM holds them once: config 4
-// ran 9.39 ms against 9.63 (2 tables) and 11.41 ms (1 table, 4 x 256 threads per SM), and
-// 9.13 ms with the PRMT-formed addresses below.
+// by lane: every lane reads its own copy, i.e. its own bank, so the 16 lookups of an AES
+// round are conflict-free whatever the state bytes are, and a column is four lookups XORed
+// with no rotates. S[x] is byte 1 of T0[x] (for AESENCLAST). The four tables (128 KiB) fit
+// once per SM, in one 1024-thread CTA (config 4: 9.39 ms against 9.63 with two tables and
+// 11.41 with one table at 4 x 256 threads per SM).
 // init[len] caches the state after the first AESENC of aes_core for len < kInitLens: it
 // depends only on (len, seed), hash.cpp:120-122.
-#ifndef PH_STR_T1
-#define PH_STR_T1 2
-#endif
 constexpr uint32_t kInitLens = 256;
-#if PH_STR_T1 > 1
 // Four tables in two 64 KiB halves: entry x of table t for lane l sits at byte
-// (t>>1)*64 KiB + x*256 + (t&1)*128 + l*4, so that one PRMT forms x*256 + l*4 (byte K of the
-// state word into byte 1, the lane offset into byte 0) and the table is an immediate offset.
+// (t>>1)*64 KiB + x*256 + (t&1)*128 + l*4 from the table base, which is placed at shared
+// address kTabBase (64 KiB-aligned): one PRMT then forms the whole shared address from the
+// state word and lw = kTabBase + l*4 (byte K of the state word into byte 1; bytes 0, 2, 3
+// from lw), and the table is the LDS immediate -- two instructions per lookup.
+constexpr uint32_t kTabBase = 0x10000;
 struct AesTables {
-    uint32_t t[4 * 256 * 32];      // 128 KiB
-    uint4 init[kInitLens];         // 4 KiB
+    uint32_t t[4 * 256 * 32];  // 128 KiB
 };
-#else
-struct AesTables {
-    uint32_t t0[256 * 32];         // 32 KiB
-#if PH_STR_T1
-    uint32_t t1[256 * 32];         // T1 = T0 rotated by 8 bits, same interleave (32 KiB)
-#endif
-    uint4 init[kInitLens];         // 4 KiB
-};
-#endif
 
 __device__ __forceinline__ uint8_t xtime(uint8_t a) {
     return (uint8_t)((a << 1) ^ ((a & 0x80) ? 0x1b : 0));
@@ -83,11 +70,6 @@ __device__ __forceinline__ uint32_t t0_entry(int x) {
     return (uint32_t)s2 | ((uint32_t)s << 8) | ((uint32_t)s << 16) | ((uint32_t)s3 << 24);
 }
 
-#if PH_STR_T1 > 1
-extern __shared__ __align__(16) uint8_t smem_raw[];  // BytesSmem, AesTables first
-__device__ __forceinline__ uint32_t tables_base() {
-    return (uint32_t)__cvta_generic_to_shared(smem_raw);
-}
 __device__ void fill_tables(AesTables& T) {
     for (int e = threadIdx.x; e < 4 * 256 * 32; e += blockDim.x) {
         const int t = e >> 13, x = (e >> 5) & 255, l = e & 31;
@@ -95,63 +77,15 @@ __device__ void fill_tables(AesTables& T) {
         T.t[((t >> 1) << 14) + (x << 6) + ((t & 1) << 5) + l] = __funnelshift_l(v, v, 8 * t);
     }
 }
-// Lookup of table TABLE at byte K of w in this lane's copy: PRMT forms byte*256 + lane*4
-// (lw = lane*4, bytes 1..3 zero), LDS reads it at the table's constant offset -- two
-// instructions per lookup. base = shared-window address of T.t.
-template <int K, int TABLE>
-__device__ __forceinline__ uint32_t tq(uint32_t base, uint32_t lw, uint32_t w) {
+// Lookup of table TABLE at byte K of w in this lane's copy (tb = kTabBase + lane*4).
+template <int K, int TABLE = 0>
+__device__ __forceinline__ uint32_t tk(uint32_t tb, uint32_t w) {
     uint32_t a, v;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(a) : "r"(w), "r"(lw), "n"(0x5504 | (K << 4)));
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v)
-                 : "r"(base + a + (uint32_t)((TABLE >> 1) * 65536 + (TABLE & 1) * 128)));
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(a) : "r"(w), "r"(tb), "n"(0x7604 | (K << 4)));
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v)
+                 : "r"(a), "n"((TABLE >> 1) * 65536 + (TABLE & 1) * 128));
     return v;
 }
-#else
-__device__ void fill_tables(AesTables& T) {
-    for (int e = threadIdx.x; e < 256 * 32; e += blockDim.x) {
-        const int x = e >> 5;
-        const uint8_t s = c_sbox[x];
-        const uint8_t s2 = xtime(s), s3 = (uint8_t)(s2 ^ s);
-        T.t0[e] = (uint32_t)s2 | ((uint32_t)s << 8) | ((uint32_t)s << 16) | ((uint32_t)s3 << 24);
-#if PH_STR_T1
-        T.t1[e] = __funnelshift_l(T.t0[e], T.t0[e], 8);
-#endif
-    }
-}
-#endif
-
-#if PH_STR_T1 > 1
-// tb = lane*4 here
-template <int K>
-__device__ __forceinline__ uint32_t tk(uint32_t tb, uint32_t w) {
-    return tq<K, 0>(tables_base(), tb, w);
-}
-template <int K, int TABLE = 1>
-__device__ __forceinline__ uint32_t tk1(uint32_t tb, uint32_t w) {
-    return tq<K, TABLE>(tables_base(), tb, w);
-}
-#else
-// Lookup of T0[byte k of w] in this lane's copy: PRMT extracts byte k, LEA forms
-// byte*128 + (this lane's table base), LDS reads it -- three instructions per lookup.
-// tb = shared-window address of T.t0 plus lane*4.
-template <int K>
-__device__ __forceinline__ uint32_t tk(uint32_t tb, uint32_t w) {
-    uint32_t byte, v;
-    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(byte) : "r"(w), "n"(0x4440 + K));
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"((byte << 7) + tb));
-    return v;
-}
-#if PH_STR_T1
-// the same lookup in table TABLE (T1..T3, TABLE x 32 KiB after T0)
-template <int K, int TABLE = 1>
-__device__ __forceinline__ uint32_t tk1(uint32_t tb, uint32_t w) {
-    uint32_t byte, v;
-    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(byte) : "r"(w), "n"(0x4440 + K));
-    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"((byte << 7) + tb), "n"(TABLE * 32768));
-    return v;
-}
-#endif
-#endif
 
 // state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
 // in-memory byte order of the __m128i in hash.cpp. AESENC = ShiftRows,
@@ -160,28 +94,11 @@ __device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4],
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-#if PH_STR_T1 > 1
-        const uint32_t a0 = tk<0>(tb, s[c]);
-        const uint32_t a1 = tk1<1, 1>(tb, s[(c + 1) & 3]);
-        const uint32_t a2 = tk1<2, 2>(tb, s[(c + 2) & 3]);
-        const uint32_t a3 = tk1<3, 3>(tb, s[(c + 3) & 3]);
+        const uint32_t a0 = tk<0, 0>(tb, s[c]);
+        const uint32_t a1 = tk<1, 1>(tb, s[(c + 1) & 3]);
+        const uint32_t a2 = tk<2, 2>(tb, s[(c + 2) & 3]);
+        const uint32_t a3 = tk<3, 3>(tb, s[(c + 3) & 3]);
         o[c] = a0 ^ a1 ^ a2 ^ a3 ^ k[c];
-#elif PH_STR_T1
-        // T0[b0] ^ T1[b1] ^ rot16(T0[b2] ^ T1[b3]): one rotate per column instead of three
-        const uint32_t a0 = tk<0>(tb, s[c]);
-        const uint32_t a1 = tk1<1>(tb, s[(c + 1) & 3]);
-        const uint32_t a2 = tk<2>(tb, s[(c + 2) & 3]);
-        const uint32_t a3 = tk1<3>(tb, s[(c + 3) & 3]);
-        const uint32_t hi = a2 ^ a3;
-        o[c] = a0 ^ a1 ^ __funnelshift_l(hi, hi, 16) ^ k[c];
-#else
-        const uint32_t a0 = tk<0>(tb, s[c]);
-        const uint32_t a1 = tk<1>(tb, s[(c + 1) & 3]);
-        const uint32_t a2 = tk<2>(tb, s[(c + 2) & 3]);
-        const uint32_t a3 = tk<3>(tb, s[(c + 3) & 3]);
-        o[c] = a0 ^ __funnelshift_l(a1, a1, 8) ^ __funnelshift_l(a2, a2, 16) ^
-               __funnelshift_l(a3, a3, 24) ^ k[c];
-#endif
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
@@ -306,13 +223,13 @@ __device__ __forceinline__ void set128(uint32_t (&s)[4], uint64_t hi, uint64_t l
 // zero-padded tail block (buf[15] ^= len - i) is the last iteration of the block loop, so a
 // key takes exactly ceil(len/16) absorbing rounds.
 __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
-                         uint64_t seed, bool wide, const DevIndex& ix, const AesTables& T,
+                         uint64_t seed, bool wide, const DevIndex& ix, const uint4* init,
                          uint32_t tb, uint64_t& hi, uint64_t& lo) {
     const uint32_t k0[4] = {ix.aes_k0[0], ix.aes_k0[1], ix.aes_k0[2], ix.aes_k0[3]};
     const uint32_t k1[4] = {ix.aes_k1[0], ix.aes_k1[1], ix.aes_k1[2], ix.aes_k1[3]};
     uint32_t s[4], w[4];
     if (len < kInitLens) {
-        const uint4 v = T.init[len];
+        const uint4 v = init[len];
         s[0] = v.x;
         s[1] = v.y;
         s[2] = v.z;
@@ -321,27 +238,44 @@ __device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_
         set128(s, (uint64_t)len * kC, seed ^ (uint64_t)len);
         aesenc(s, k0, tb);
     }
-    // The key's bytes arrive as aligned 16-byte granules g0..gl, prefetched one block ahead
-    // (block b needs granules b and b+1; granule b+2 is loaded while block b is hashed).
-    // No granule past gl is read, i.e. no access leaves the granules covering the key.
+    // Block b's 16 bytes are words 4b..4b+4 of the key's 4-byte-aligned span, shifted by
+    // the key's start offset in its first word (one funnel shift per output word, no
+    // selects). Only words that hold a byte of the key are read. The blocks every active
+    // lane has in full run unmasked; the rest (each lane's zero-padded tail block, and the
+    // full blocks of lanes with more than the warp's minimum) run masked.
     const uint32_t nblk = (len + 15) >> 4;
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + off);
-    const uint4* gp = reinterpret_cast<const uint4*>(a0 & ~uintptr_t{15});
-    const uint32_t sh = (uint32_t)(a0 & 15);
-    const uint32_t gl = len ? (sh + len - 1) >> 4 : 0;
-    const uint4 zero = make_uint4(0, 0, 0, 0);
-    uint4 cur = nblk ? __ldg(gp) : zero;
-    uint4 nxt = gl >= 1 ? __ldg(gp + 1) : zero;
-    for (uint32_t b = 0; b < nblk; b++) {
-        const uint4 nn = b + 2 <= gl ? __ldg(gp + b + 2) : zero;  // prefetch
-        const uint32_t rem = len - (b << 4);
-        realign16(cur, nxt, sh, rem, w);
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(a0 & ~uintptr_t{3});
+    const uint32_t sh4 = (uint32_t)(a0 & 3), rs = sh4 * 8;
+    const uint32_t nfull = __reduce_min_sync(__activemask(), len >> 4);
+    uint32_t b = 0;
+    for (; b < nfull; b++) {
+        const uint32_t* q = wp + 4 * b;
+        const uint32_t v0 = __ldg(q), v1 = __ldg(q + 1), v2 = __ldg(q + 2), v3 = __ldg(q + 3);
+        const uint32_t v4 = sh4 ? __ldg(q + 4) : 0;
+        s[0] ^= __funnelshift_r(v0, v1, rs);
+        s[1] ^= __funnelshift_r(v1, v2, rs);
+        s[2] ^= __funnelshift_r(v2, v3, rs);
+        s[3] ^= __funnelshift_r(v3, v4, rs);
+        aesenc(s, k1, tb);
+    }
+    for (; b < nblk; b++) {
+        const uint32_t rem = len - (b << 4);  // bytes left: >= 16, or the tail's 1..15
+        const uint32_t nw = (sh4 + (rem < 16 ? rem : 16) + 3) >> 2;  // words holding key bytes
+        const uint32_t* q = wp + 4 * b;
+        uint32_t v[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) v[i] = (uint32_t)i < nw ? __ldg(q + i) : 0;
+        const int base = 32 - 8 * (int)rem;  // word t keeps rem - 4t bytes
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const uint32_t m = __funnelshift_rc(0xffffffffu, 0u, (uint32_t)max(base + 32 * t, 0));
+            w[t] = __funnelshift_r(v[t], v[t + 1], rs) & m;
+        }
         if (rem < 16) w[3] ^= rem << 24;  // buf[15] ^= len - i
 #pragma unroll
         for (int c = 0; c < 4; c++) s[c] ^= w[c];
         aesenc(s, k1, tb);
-        cur = nxt;
-        nxt = nn;
     }
     aesenc(s, k0, tb);
     aesenc(s, k1, tb);
@@ -368,31 +302,33 @@ constexpr int kBytesThreads = PH_STR_THREADS;
 constexpr int kBytesWarps = kBytesThreads / 32;
 constexpr uint32_t kClasses = 8;  // block counts 0..6, and 7 for >= 7 blocks
 
-struct BytesSmem {  // dynamic shared memory of k_query_bytes
-    AesTables T;
+// Dynamic shared memory of k_query_bytes: BytesLow from the start of the window, the AES
+// tables at shared address kTabBase (so the allocation spans kTabBase + 128 KiB minus the
+// window's start; BytesLow must end below kTabBase, checked at run time).
+struct BytesLow {
+    uint4 init[kInitLens];                  // states after the first AESENC, by length
     uint64_t off[kBytesWarps][kBatch + 1];  // each warp batch's offsets
     uint8_t perm[kBytesWarps][kBatch];      // the batch in block-count order
 };
+constexpr size_t kBytesSmem = kTabBase + sizeof(AesTables);  // 192 KiB
 
 template <int G, bool POW2, class OutT>
-__global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix,
+__global__ void __launch_bounds__(kBytesThreads, 1) k_query_bytes(const DevIndex ix,
                                                      const uint8_t* __restrict__ data,
                                                      const uint64_t* __restrict__ offsets,
                                                      uint64_t base_off, OutT* __restrict__ out, uint64_t nkeys,
                                                      int minimal) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    BytesSmem& SM = *reinterpret_cast<BytesSmem*>(smem_raw);
-    AesTables& T = SM.T;
+    const uint32_t win = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    if (win + sizeof(BytesLow) > kTabBase) __trap();  // (the window starts at <= 1 KiB)
+    BytesLow& SM = *reinterpret_cast<BytesLow*>(smem_raw);
+    AesTables& T = *reinterpret_cast<AesTables*>(smem_raw + (kTabBase - win));
     auto& s_off = SM.off;
     auto& s_perm = SM.perm;
     const int algo = ix.hash_algo;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1;
-#if PH_STR_T1 > 1
-    const uint32_t tb = lane * 4;
-#else
-    const uint32_t tb = (uint32_t)__cvta_generic_to_shared(T.t0) + lane * 4;
-#endif
+    const uint32_t tb = kTabBase + lane * 4;
     if (algo == 1 || algo == 2) {
         fill_tables(T);
         __syncthreads();
@@ -401,7 +337,7 @@ __global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix
             uint32_t st[4];
             set128(st, (uint64_t)len * kC, ix.seed ^ (uint64_t)len);  // hash.cpp:120-122
             aesenc(st, k0, tb);
-            T.init[len] = make_uint4(st[0], st[1], st[2], st[3]);
+            SM.init[len] = make_uint4(st[0], st[1], st[2], st[3]);
         }
         __syncthreads();
     }
@@ -454,7 +390,7 @@ __global__ void __launch_bounds__(kBytesThreads) k_query_bytes(const DevIndex ix
                 const uint64_t o0 = so[e] - base_off, o1 = so[e + 1] - base_off;
                 const uint32_t len = (uint32_t)(o1 - o0);
                 if (algo == 1 || algo == 2) {
-                    aes_hash(data, o0, len, ix.seed, algo == 2, ix, T, tb, hi, lo);
+                    aes_hash(data, o0, len, ix.seed, algo == 2, ix, SM.init, tb, hi, lo);
                 } else if (algo == 4) {
                     hi = portable_hash64(data, o0, len, ix.seed ^ kP3);
                     lo = portable_hash64(data, o0, len, mix64(ix.seed) + kGolden);
@@ -490,7 +426,7 @@ template <int G, bool POW2, class OutT>
 static cudaError_t launch_b(const DevIndex& ix, const uint8_t* d, const uint64_t* o,
                             uint64_t bo, void* out, uint64_t n, int minimal, cudaStream_t s, int sms) {
     auto kern = k_query_bytes<G, POW2, OutT>;
-    constexpr size_t smem = sizeof(BytesSmem);
+    constexpr size_t smem = kBytesSmem;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int bps = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kBytesThreads, smem) != cudaSuccess ||

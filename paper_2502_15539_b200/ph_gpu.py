@@ -73,6 +73,8 @@ _L.ph_gpu_set_launch.argtypes = [C.c_int, C.c_int]
 _L.ph_gpu_set_partition.argtypes = [C.c_int]
 _L.ph_gpu_set_regime.argtypes = [C.c_int]
 _L.ph_gpu_index_set_l2_policy.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
+_L.ph_gpu_index_set_scratch_limit.argtypes = [C.c_void_p, C.c_uint64]
+_L.ph_gpu_gather_replay_u64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
 
 # status codes (ph_gpu.h)
 OK, E_INVALID, E_FORMAT, E_CUDA, E_KEYKIND, E_NOMEM, E_UNSUPPORTED = range(7)
@@ -160,10 +162,75 @@ def _is_torch(x):
 
 
 def _stream_ptr(stream):
-    if stream is not None:
-        return C.c_void_p(int(stream))
-    import torch
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    """None (torch's current stream), a torch.cuda.Stream, or a raw cudaStream_t (int)."""
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+_WORD_DTYPES = ("int64", "uint64")
+
+
+def _dtype_name(x) -> str:
+    return str(x.dtype).replace("torch.", "")
+
+
+def _contiguous(x) -> bool:
+    return x.is_contiguous() if _is_torch(x) else bool(x.flags["C_CONTIGUOUS"])
+
+
+def _count(x) -> int:
+    return x.numel() if _is_torch(x) else x.size
+
+
+def _check_words(x, what: str, min_count: int):
+    """x: a contiguous 64-bit-word array (torch or numpy) with at least min_count entries."""
+    if _dtype_name(x) not in _WORD_DTYPES:
+        raise ValueError(f"{what} must hold 64-bit words (int64/uint64), got {x.dtype}")
+    if not _contiguous(x):
+        raise ValueError(f"{what} must be contiguous")
+    if _count(x) < min_count:
+        raise ValueError(f"{what} holds {_count(x)} entries, needs {min_count}")
+
+
+def _check_out(out, n: int, out_width: int, cuda: bool):
+    """A caller-supplied output: out_width bytes per element, >= n elements, contiguous and
+    in the same residence (device or host) as the inputs."""
+    if out_width not in (4, 8):
+        raise ValueError("out_width must be 4 or 8")
+    if out is None:
+        return
+    if _is_torch(out):
+        if bool(out.is_cuda) != cuda:
+            raise ValueError("out must live where the keys live (device or host)")
+        size = out.element_size()
+    else:
+        if cuda:
+            raise ValueError("out must be a CUDA tensor for device-resident keys")
+        if not isinstance(out, np.ndarray):
+            raise ValueError("a host out must be a numpy array or a CPU tensor")
+        size = out.itemsize
+    if size != out_width:
+        raise ValueError(f"out has {size}-byte elements but out_width is {out_width}")
+    if _count(out) < n:
+        raise ValueError(f"out holds {_count(out)} elements, needs {n}")
+    if not _contiguous(out):
+        raise ValueError("out must be contiguous")
+
+
+def _new_out(n: int, out_width: int, like):
+    if _is_torch(like) and like.is_cuda:
+        import torch
+        return torch.empty(n, dtype=torch.int32 if out_width == 4 else torch.int64,
+                           device=like.device)
+    return np.empty(n, dtype=np.uint32 if out_width == 4 else np.uint64)
+
+
+def _host(x):
+    return x.numpy() if _is_torch(x) else x
 
 
 class PtrHashIndex:
@@ -212,6 +279,10 @@ class PtrHashIndex:
     def trim(self):
         """Release the index's cached per-call scratch (ph_gpu_index_trim)."""
         _check(_L.ph_gpu_index_trim(self._h))
+
+    def set_scratch_limit(self, nbytes: int):
+        """Ceiling on cached per-call scratch (ph_gpu_index_set_scratch_limit)."""
+        _check(_L.ph_gpu_index_set_scratch_limit(self._h, int(nbytes)))
 
     def set_l2_policy(self, hot_bytes: int, flags: int = 0):
         """Pilot layout / L2 policy (ph_gpu_index_set_l2_policy); results are unaffected."""
@@ -274,71 +345,89 @@ class PtrHashIndex:
         return self.query(keys, out, minimal, out_width, stream)
 
     def query(self, keys, out=None, minimal=True, out_width=4, stream=None):
-        """out[i] = index(keys[i]) (minimal) or index_no_remap(keys[i])."""
-        if out_width not in (4, 8):
-            raise ValueError("out_width must be 4 or 8")
+        """out[i] = index(keys[i]) (minimal) or index_no_remap(keys[i]). Raises ValueError
+        on a key dtype other than int64/uint64, a non-contiguous array, or an `out` of the
+        wrong element width, size or residence."""
         if isinstance(keys, tuple):
             return self._query_bytes(keys[0], keys[1], out, minimal, out_width, stream)
-        if _is_torch(keys) and keys.is_cuda:
-            import torch
-            n = keys.numel()
-            if out is None:
-                out = torch.empty(n, dtype=torch.int32 if out_width == 4 else torch.int64,
-                                  device=keys.device)
-            assert keys.is_contiguous() and out.is_contiguous() and out.numel() >= n
+        cuda = _is_torch(keys) and keys.is_cuda
+        if not _is_torch(keys):
+            keys = np.asarray(keys)
+        n = _count(keys)
+        _check_words(keys, "keys", n)
+        _check_out(out, n, out_width, cuda)
+        if out is None:
+            out = _new_out(n, out_width, keys)
+        if cuda:
             _check(_L.ph_gpu_query_u64(self._h, C.c_void_p(keys.data_ptr()), n,
                                        C.c_void_p(out.data_ptr()), out_width, int(minimal),
                                        _stream_ptr(stream)))
             return out
-        k = keys.numpy() if _is_torch(keys) else keys
-        k = np.ascontiguousarray(k).view(np.uint64) if k.dtype != np.uint64 else np.ascontiguousarray(k)
-        if out is None:
-            out = np.empty(k.size, dtype=np.uint32 if out_width == 4 else np.uint64)
-        o = out.numpy() if _is_torch(out) else out
-        _check(_L.ph_gpu_index_stream_u64(self._h, C.c_void_p(k.ctypes.data), k.size,
+        k, o = _host(keys), _host(out)
+        _check(_L.ph_gpu_index_stream_u64(self._h, C.c_void_p(k.ctypes.data), n,
                                           C.c_void_p(o.ctypes.data), out_width, int(minimal)))
         return out
+
+    def gather_replay(self, keys, stream=None):
+        """Measurement: the pilot reads alone at the true bucket addresses of the CUDA u64
+        tensor `keys` (ph_gpu_gather_replay_u64; bench.py's replay bound)."""
+        if not (_is_torch(keys) and keys.is_cuda):
+            raise ValueError("gather_replay takes a CUDA tensor")
+        _check_words(keys, "keys", keys.numel())
+        _check(_L.ph_gpu_gather_replay_u64(self._h, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                           _stream_ptr(stream)))
 
     def query_kmers(self, seq, n_bases: int, k: int = 31, out=None, minimal=True, out_width=4,
                     stream=None):
         """Fused k-mer queries: out[i] = index(kmer_i(seq)) for i < n_bases-k+1 (ph_gpu.h
-        ph_gpu_query_kmers). `seq` is the 2-bit packed MSB-first sequence (u64 words)."""
+        ph_gpu_query_kmers). `seq` is the 2-bit packed MSB-first sequence (u64 words, at
+        least ceil(n_bases/32) of them)."""
+        if not 1 <= k <= 32:
+            raise ValueError("k must be in [1, 32]")
         n = max(0, n_bases - k + 1)
-        if _is_torch(seq) and seq.is_cuda:
-            import torch
-            if out is None:
-                out = torch.empty(n, dtype=torch.int32 if out_width == 4 else torch.int64,
-                                  device=seq.device)
+        cuda = _is_torch(seq) and seq.is_cuda
+        if not _is_torch(seq):
+            seq = np.asarray(seq)
+        _check_words(seq, "seq", (n_bases + 31) // 32)
+        _check_out(out, n, out_width, cuda)
+        if out is None:
+            out = _new_out(n, out_width, seq)
+        if cuda:
             _check(_L.ph_gpu_query_kmers(self._h, C.c_void_p(seq.data_ptr()), n_bases, k,
                                          C.c_void_p(out.data_ptr()), out_width, int(minimal),
                                          _stream_ptr(stream)))
             return out
-        s = seq.numpy() if _is_torch(seq) else np.ascontiguousarray(seq)
-        if out is None:
-            out = np.empty(n, dtype=np.uint32 if out_width == 4 else np.uint64)
-        o = out.numpy() if _is_torch(out) else out
-        _check(_L.ph_gpu_index_stream_kmers(self._h, C.c_void_p(s.ctypes.data), n_bases, k,
+        s_, o = _host(seq), _host(out)
+        _check(_L.ph_gpu_index_stream_kmers(self._h, C.c_void_p(s_.ctypes.data), n_bases, k,
                                             C.c_void_p(o.ctypes.data), out_width, int(minimal)))
         return out
 
     def _query_bytes(self, data, offsets, out, minimal, out_width, stream):
-        if _is_torch(data) and data.is_cuda:
-            import torch
-            n = offsets.numel() - 1
-            if out is None:
-                out = torch.empty(n, dtype=torch.int32 if out_width == 4 else torch.int64,
-                                  device=data.device)
+        cuda = _is_torch(data) and data.is_cuda
+        if (_is_torch(offsets) and offsets.is_cuda) != cuda:
+            raise ValueError("bytes and offsets must both be on the device or both on the host")
+        if not _is_torch(data):
+            data = np.asarray(data)
+        if not _is_torch(offsets):
+            offsets = np.asarray(offsets)
+        if _dtype_name(data) not in ("uint8", "int8"):
+            raise ValueError(f"string bytes must be uint8, got {data.dtype}")
+        if not _contiguous(data):
+            raise ValueError("string bytes must be contiguous")
+        if _count(offsets) < 1:
+            raise ValueError("offsets must hold n+1 entries")
+        n = _count(offsets) - 1
+        _check_words(offsets, "offsets", n + 1)
+        _check_out(out, n, out_width, cuda)
+        if out is None:
+            out = _new_out(n, out_width, data)
+        if cuda:
             _check(_L.ph_gpu_query_bytes(self._h, C.c_void_p(data.data_ptr()),
                                          C.c_void_p(offsets.data_ptr()), n,
                                          C.c_void_p(out.data_ptr()), out_width, int(minimal),
                                          _stream_ptr(stream)))
             return out
-        d = data.numpy() if _is_torch(data) else np.ascontiguousarray(data, dtype=np.uint8)
-        o_ = offsets.numpy() if _is_torch(offsets) else np.ascontiguousarray(offsets, dtype=np.uint64)
-        n = o_.size - 1
-        if out is None:
-            out = np.empty(n, dtype=np.uint32 if out_width == 4 else np.uint64)
-        oo = out.numpy() if _is_torch(out) else out
+        d, o_, oo = _host(data), _host(offsets), _host(out)
         if d.size == 0:
             d = np.zeros(1, dtype=np.uint8)
         _check(_L.ph_gpu_index_stream_bytes(self._h, C.c_void_p(d.ctypes.data),

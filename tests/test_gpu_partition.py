@@ -1,4 +1,4 @@
-"""GPU tests of the partitioned query path (ph_bins.cu): forced on for
+"""GPU tests of the partitioned query path (csrc/ph_partition.cu): forced on for
 small indexes (ph_gpu_set_partition(2)), its outputs must equal the reference's for u64
 keys and k-mers, u32/u64 outputs, minimal/non-minimal, every bucket function / reduce /
 remap encoding of the golden fixtures, and ragged batch sizes."""

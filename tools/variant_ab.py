@@ -24,12 +24,28 @@ def child(a):
     from paper_2502_15539_b200 import ph_gpu
     from tools.synth_perf import SHAPES, synth_ptrh
     ptrh = synth_ptrh(a.config)
+    if a.strings:  # the same shape as a string index hashed with aes64 (header bytes 8, 9)
+        ptrh = ptrh[:8] + bytes([1, 1]) + ptrh[10:]
     idx = ph_gpu.PtrHashIndex(ptrh)
     idx.set_l2_policy(0, 2)  # file order, no window: DRAM-sized batches take the partitioned path
-    n = SHAPES[a.config][0]
+    n = a.nq or SHAPES[a.config][0]
     g = torch.Generator(device="cuda")
     g.manual_seed(7)
-    if a.kmers:
+    if a.strings:  # config-4 strings (len U[8,64], bytes 0x21-0x7E), shuffled, device-generated
+        import ctypes as C
+        bench = C.CDLL(os.path.join(ROOT, "paper_2502_15539_b200", "libph_bench.so"))
+        lens = torch.empty(n, dtype=torch.int64, device="cuda")
+        assert bench.phb_str_lens(C.c_void_p(lens.data_ptr()), C.c_uint64(n), C.c_uint64(43),
+                                  C.c_uint64(7), 1, None) == 0
+        offs = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+        torch.cumsum(lens, 0, out=offs[1:])
+        del lens
+        data = torch.empty(int(offs[-1].item()), dtype=torch.uint8, device="cuda")
+        assert bench.phb_str_bytes(C.c_void_p(offs.data_ptr()), C.c_uint64(n), C.c_uint64(43),
+                                   C.c_uint64(7), 1, C.c_void_p(data.data_ptr()), None) == 0
+        torch.cuda.synchronize()
+        run = lambda out, m: idx.query((data, offs), out=out, minimal=m, out_width=4)  # noqa
+    elif a.kmers:
         nb = n + 30
         seq = torch.randint(-2**63, 2**63 - 1, ((nb + 31) // 32,), dtype=torch.int64,
                             device="cuda", generator=g)
@@ -40,6 +56,12 @@ def child(a):
     out = torch.empty(n, dtype=torch.int32, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     res = {}
+    if a.ncu:  # one call per mode for the profiler, no timing
+        for minimal in (True, False):
+            run(out, minimal)
+        torch.cuda.synchronize()
+        print("RESULT {}", flush=True)
+        return
     for minimal in (True, False):
         for _ in range(3):
             run(out, minimal)
@@ -71,6 +93,9 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--repeat", type=int, default=1, help="interleaved repetitions of the list")
     ap.add_argument("--kmers", action="store_true")
+    ap.add_argument("--strings", action="store_true", help="config-4 strings on an aes64 index")
+    ap.add_argument("--nq", type=int, default=0, help="queries (default: the shape's n)")
+    ap.add_argument("--ncu", action="store_true", help="child only: one call per mode")
     ap.add_argument("--child", action="store_true")
     a = ap.parse_args()
     if a.child:
@@ -87,7 +112,8 @@ def main():
                 k, v = item.split("=", 1)
                 env[k] = v
             cmd = [sys.executable, __file__, "--child", "--config", str(a.config), "--runs", "-",
-                   "--reps", str(a.reps)] + (["--kmers"] if a.kmers else [])
+                   "--reps", str(a.reps), "--nq", str(a.nq)] + (["--kmers"] if a.kmers else []) + \
+                (["--strings"] if a.strings else [])
             p = subprocess.run(cmd, env=env, capture_output=True, text=True)
             line = [x for x in p.stdout.splitlines() if x.startswith("RESULT ")]
             if p.returncode or not line:

@@ -55,12 +55,14 @@ def build_lib(name, sources, extra=(), log=None, force=False):
         return out
     objdir = os.path.join(PKG, "build", os.path.basename(name)[:-3])
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for s in srcs:
-        o = os.path.join(objdir, os.path.basename(s) + ".o")
-        _run([nvcc(), *ARCH, *NVFLAGS, *extra, "-I", CSRC, "-I", os.path.join(ROOT, "include"),
-              "-c", s, "-o", o], log)
-        objs.append(o)
+    objs = [os.path.join(objdir, os.path.basename(s) + ".o") for s in srcs]
+    from concurrent.futures import ThreadPoolExecutor  # one nvcc per source, in parallel
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        futs = [ex.submit(_run, [nvcc(), *ARCH, *NVFLAGS, *extra, "-I", CSRC, "-I",
+                                 os.path.join(ROOT, "include"), "-c", s, "-o", o], log)
+                for s, o in zip(srcs, objs)]
+        for f in futs:
+            f.result()
     _run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", out, *objs], log)
     return out
 

@@ -119,6 +119,7 @@ struct ph_gpu_index {
     void* d_remap = nullptr;
     void* d_ef[3] = {nullptr, nullptr, nullptr};
     void* d_opt = nullptr;
+    void* d_aes = nullptr;  // AES T-tables (string indexes, small batches)
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch for the deferred remap
     // host-path pipelines (streams + staging buffers), reused across calls
     mutable std::mutex pl_mu;
@@ -381,6 +382,7 @@ void release(ph_gpu_index* ix) {
     cudaFree(ix->d_remap);
     for (void* p : ix->d_ef) cudaFree(p);
     cudaFree(ix->d_opt);
+    cudaFree(ix->d_aes);
     if (ix->pool) cudaMemPoolDestroy(ix->pool);
     delete ix;
 }
@@ -596,11 +598,18 @@ int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_inde
         optimal_table(t);
         rc = upload(t.data(), t.size() * 8, &ix->d_opt);
     }
+    if (!rc && p.key_kind == 1) {
+        cudaError_t e = cudaMalloc(&ix->d_aes, 4096);
+        if (e == cudaSuccess) e = phg::launch_fill_aes_tab(static_cast<uint32_t*>(ix->d_aes), nullptr);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+        if (e != cudaSuccess) rc = cuda_fail(e, "AES table upload");
+    }
     if (rc) {
         release(ix);
         return rc;
     }
     phg::DevIndex& d = ix->dev;
+    d.aes_tab = static_cast<const uint32_t*>(ix->d_aes);
     d.pilots = static_cast<const uint8_t*>(ix->d_pilots);
     d.remap = static_cast<const uint8_t*>(ix->d_remap);
     d.ef_low = static_cast<const uint64_t*>(ix->d_ef[0]);
@@ -1137,10 +1146,10 @@ int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uin
     return PH_OK;
 }
 
-// Single-key queries (index.hpp:60-64), synchronous: the key is written into the index's
-// mapped pinned block, one kernel launch reads it and writes the answer back in place, and
-// the call waits on the index's single-key stream. Many host threads may call at once; they
-// take turns on the block.
+// Single-key queries (index.hpp:60-64), synchronous: one kernel launch takes the key as a
+// launch parameter (string keys up to 256 bytes; longer ones are written into the index's mapped
+// pinned block) and writes the answer into that block, and the call waits on the index's
+// single-key stream. Many host threads may call at once; they take turns on the block.
 int ph_gpu_index_u64(const ph_gpu_index* ix, uint64_t key, int minimal, uint64_t* out) {
     if (!ix || !out) return fail(PH_E_INVALID, "null argument");
     if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
@@ -1150,9 +1159,8 @@ int ph_gpu_index_u64(const ph_gpu_index* ix, uint64_t key, int minimal, uint64_t
     if (int rc = ensure_single(ix, 0)) return rc;
     auto* h = reinterpret_cast<volatile uint64_t*>(ix->single_h);
     auto* d = reinterpret_cast<uint64_t*>(ix->single_d);
-    h[0] = key;
-    cudaError_t e = phg::launch_query_u64(ix->dev, ix->info.bucket_fn, ix->info.pow2, d, d + 2, 8,
-                                          1, minimal, ix->single_s, ix->sms);
+    cudaError_t e = phg::launch_index_u64_one(ix->dev, ix->info.bucket_fn, ix->info.pow2, key,
+                                              d + 2, minimal, ix->single_s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ix->single_s);
     if (e != cudaSuccess) return cuda_fail(e, "index_u64");
     *out = h[2];
@@ -1166,9 +1174,18 @@ int ph_gpu_index_bytes(const ph_gpu_index* ix, const uint8_t* key, size_t len, i
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     std::lock_guard<std::mutex> lk(ix->single_mu);
-    if (int rc = ensure_single(ix, len)) return rc;
+    if (int rc = ensure_single(ix, len <= 256 ? 0 : len)) return rc;
     auto* h = reinterpret_cast<volatile uint64_t*>(ix->single_h);
     auto* d = reinterpret_cast<uint64_t*>(ix->single_d);
+    if (len <= 256) {  // the key rides in the launch parameters: no host read by the kernel
+        cudaError_t e = phg::launch_index_bytes_one(ix->dev, ix->info.bucket_fn, ix->info.pow2,
+                                                    key, static_cast<uint32_t>(len), d + 2,
+                                                    minimal, ix->single_s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ix->single_s);
+        if (e != cudaSuccess) return cuda_fail(e, "index_bytes");
+        *out = h[2];
+        return PH_OK;
+    }
     h[0] = 0;  // offsets {0, len}; the bytes follow the header
     h[1] = len;
     if (len) std::memcpy(ix->single_h + kSingleHeader, key, len);

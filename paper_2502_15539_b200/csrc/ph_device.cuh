@@ -57,6 +57,7 @@ struct DevIndex {
     int32_t pilot_evict_normal;   // 1: pilot loads L2::evict_normal instead of evict_last (A/B knob)
     // AES string hash round keys k0/k1 (hash.cpp:116-119) as LE u32 words, host-derived
     uint32_t aes_k0[4], aes_k1[4];
+    const uint32_t* aes_tab;      // T0..T3 (4 x 256 words) in global memory (small batches)
 };
 
 // Device address of pilots[part*B + bucket] under the hot-first layout.
@@ -188,10 +189,10 @@ static __device__ __noinline__ uint32_t bucket_exact(uint64_t x, uint32_t B,
     uint64_t unused;
     return (uint32_t)mul32x64(B, gamma<G>(x, opt), unused);
 }
-template <int G>
+template <int G, bool FAST = !PH_NO_FAST_BUCKET>
 __device__ __forceinline__ uint32_t bucket_of(uint64_t x, uint32_t B,
                                               const uint64_t* __restrict__ opt) {
-    if constexpr (G <= 2 && !PH_NO_FAST_BUCKET) {
+    if constexpr (G <= 2 && FAST) {
         bool ok;
         const uint32_t b = bucket_fast<G>((uint32_t)(x >> 32), B, ok);
         if (__builtin_expect(ok, 1)) return b;

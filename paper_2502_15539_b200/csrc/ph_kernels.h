@@ -61,6 +61,15 @@ cudaError_t launch_query_bytes(const DevIndex& ix, int gamma_kind, bool pow2,
                                void* out, int out_width, uint64_t n, int minimal, cudaStream_t s,
                                int sms);
 
+cudaError_t launch_fill_aes_tab(uint32_t* tab, cudaStream_t s);
+// One u64 key as a launch parameter (single-key index()).
+cudaError_t launch_index_u64_one(const DevIndex& ix, int gamma_kind, bool pow2, uint64_t key,
+                                 uint64_t* out, int minimal, cudaStream_t s);
+// One string key of at most 256 bytes, passed in the launch parameters (single-key index()).
+cudaError_t launch_index_bytes_one(const DevIndex& ix, int gamma_kind, bool pow2,
+                                   const uint8_t* key, uint32_t len, uint64_t* out, int minimal,
+                                   cudaStream_t s);
+
 cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, const uint64_t* seq,
                                uint64_t n_bases, int k, void* out, int out_width, int minimal,
                                cudaStream_t s, int sms,

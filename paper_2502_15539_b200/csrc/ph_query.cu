@@ -348,6 +348,43 @@ cudaError_t launch_query_kmers(const DevIndex& ix, int gamma_kind, bool pow2, co
                       out, out_width, n, minimal, s, sms, rl);
 }
 
+// index(key) / index_no_remap(key) for one u64 key (ph_gpu_index_u64): the key is a launch
+// parameter and one thread answers it (slot_of + remap_slot, index.hpp:91-100).
+template <int G, bool POW2>
+__global__ void __launch_bounds__(32) k_index_u64_one(const DevIndex ix, uint64_t key,
+                                                      uint64_t* __restrict__ out, int minimal) {
+    if (threadIdx.x) return;
+    const uint64_t h = kC * (key ^ ix.seed);  // hash_int, hash.hpp:27
+    uint64_t x;
+    const uint32_t part = (uint32_t)mul32x64((uint32_t)ix.P, h, x);
+    const uint32_t bucket = bucket_of<G>(x, (uint32_t)ix.B, ix.opt_table);
+    const uint32_t pilot = ix.pilots[pilot_offset(ix, part, bucket)];
+    uint64_t slot = (uint64_t)part * (uint32_t)ix.S + reduce<POW2>(ix, h ^ hash_pilot(ix, pilot));
+    if (minimal && slot >= ix.n) slot = remap_get(ix, slot - ix.n);
+    *out = slot;
+}
+
+cudaError_t launch_index_u64_one(const DevIndex& ix, int gamma_kind, bool pow2, uint64_t key,
+                                 uint64_t* out, int minimal, cudaStream_t s) {
+#define PH_CASE(G)                                                                         \
+    case G:                                                                                \
+        if (pow2) k_index_u64_one<G, true><<<1, 32, 0, s>>>(ix, key, out, minimal);       \
+        else k_index_u64_one<G, false><<<1, 32, 0, s>>>(ix, key, out, minimal);           \
+        break;
+    switch (gamma_kind) {
+        PH_CASE(0)
+        PH_CASE(1)
+        PH_CASE(2)
+        PH_CASE(3)
+        PH_CASE(4)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef PH_CASE
+    note_launch();
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // Gather-only replay (measurement: bench.py's replay bound). The pilot reads of
 // the query path at the index's true bucket addresses, in the order of `keys`, with the same

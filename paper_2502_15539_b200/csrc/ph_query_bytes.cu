@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 #include "ph_device.cuh"
 #include "ph_kernels.h"
@@ -78,37 +79,68 @@ __device__ void fill_tables(AesTables& T) {
     }
 }
 // Lookup of table TABLE at byte K of w in this lane's copy (tb = kTabBase + lane*4).
-template <int K, int TABLE = 0>
-__device__ __forceinline__ uint32_t tk(uint32_t tb, uint32_t w) {
-    uint32_t a, v;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(a) : "r"(w), "r"(tb), "n"(0x7604 | (K << 4)));
-    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v)
-                 : "r"(a), "n"((TABLE >> 1) * 65536 + (TABLE & 1) * 128));
-    return v;
+struct SmemLook {
+    uint32_t tb;
+    template <int K, int TABLE>
+    __device__ __forceinline__ uint32_t get(uint32_t w) const {
+        uint32_t a, v;
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(a) : "r"(w), "r"(tb), "n"(0x7604 | (K << 4)));
+        asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v)
+                     : "r"(a), "n"((TABLE >> 1) * 65536 + (TABLE & 1) * 128));
+        return v;
+    }
+};
+// The same four tables, one copy each, staged in shared memory by a small launch (few lanes,
+// so bank conflicts do not matter; one round trip to L2 for the whole 4 KiB instead of one
+// per dependent AES round).
+struct FlatLook {
+    const uint32_t* tab;  // shared memory
+    template <int K, int TABLE>
+    __device__ __forceinline__ uint32_t get(uint32_t w) const {
+        return tab[TABLE * 256 + ((w >> (8 * K)) & 255)];
+    }
+};
+__device__ __forceinline__ void stage_aes_tab(uint32_t* dst, const uint32_t* __restrict__ src) {
+    for (uint32_t i = threadIdx.x; i < 1024 / 4; i += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// 16-byte load of key bytes: read-only global path, or (GEN) a generic load, for keys
+// staged in shared memory (k_index_bytes_one).
+template <bool GEN>
+__device__ __forceinline__ uint4 ldq(const uint4* p) {
+    if constexpr (GEN) return *p;
+    else return __ldg(p);
 }
 
 // state: 4 little-endian u32 columns (byte 4c+r = row r of column c), i.e. the
 // in-memory byte order of the __m128i in hash.cpp. AESENC = ShiftRows,
 // SubBytes, MixColumns, AddRoundKey (Intel semantics).
-__device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4], uint32_t tb) {
+template <class L>
+__device__ __forceinline__ void aesenc(uint32_t (&s)[4], const uint32_t (&k)[4], const L& T) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        const uint32_t a0 = tk<0, 0>(tb, s[c]);
-        const uint32_t a1 = tk<1, 1>(tb, s[(c + 1) & 3]);
-        const uint32_t a2 = tk<2, 2>(tb, s[(c + 2) & 3]);
-        const uint32_t a3 = tk<3, 3>(tb, s[(c + 3) & 3]);
+        const uint32_t a0 = T.template get<0, 0>(s[c]);
+        const uint32_t a1 = T.template get<1, 1>(s[(c + 1) & 3]);
+        const uint32_t a2 = T.template get<2, 2>(s[(c + 2) & 3]);
+        const uint32_t a3 = T.template get<3, 3>(s[(c + 3) & 3]);
         o[c] = a0 ^ a1 ^ a2 ^ a3 ^ k[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) s[c] = o[c];
 }
-__device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)[4], uint32_t tb) {
+template <class L>
+__device__ __forceinline__ void aesenclast(uint32_t (&s)[4], const uint32_t (&k)[4], const L& T) {
     uint32_t o[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        const uint32_t a0 = tk<0>(tb, s[c]), a1 = tk<1>(tb, s[(c + 1) & 3]);
-        const uint32_t a2 = tk<2>(tb, s[(c + 2) & 3]), a3 = tk<3>(tb, s[(c + 3) & 3]);
+        const uint32_t a0 = T.template get<0, 0>(s[c]), a1 = T.template get<1, 0>(s[(c + 1) & 3]);
+        const uint32_t a2 = T.template get<2, 0>(s[(c + 2) & 3]), a3 = T.template get<3, 0>(s[(c + 3) & 3]);
         // S[x] is byte 1 of T0[x]: gather byte 1 of a0..a3 into bytes 0..3
         uint32_t lo, hi, v;
         asm("prmt.b32 %0, %1, %2, 0x0051;" : "=r"(lo) : "r"(a0), "r"(a1));  // bytes 0,1
@@ -148,14 +180,15 @@ __device__ __forceinline__ void realign16(const uint4& lo, const uint4& hi, uint
 // Loads min(avail,16) bytes at base+off as 4 LE words, zero past `avail`, with at most
 // two aligned 16-byte loads. Only aligned 16-byte granules that hold at least one
 // requested byte are read, so no access leaves the granules covering the key.
+template <bool GEN>
 __device__ __forceinline__ void load16(const uint8_t* __restrict__ base, uint64_t off,
                                        uint32_t avail, uint32_t (&w)[4]) {
     const uintptr_t addr = reinterpret_cast<uintptr_t>(base + off);
     const uint4* p = reinterpret_cast<const uint4*>(addr & ~uintptr_t{15});
     const uint32_t sh = (uint32_t)(addr & 15);
     const uint32_t nb = avail < 16 ? avail : 16;
-    const uint4 lo = __ldg(p);
-    const uint4 hi = (sh + nb > 16) ? __ldg(p + 1) : make_uint4(0, 0, 0, 0);
+    const uint4 lo = ldq<GEN>(p);
+    const uint4 hi = (sh + nb > 16) ? ldq<GEN>(p + 1) : make_uint4(0, 0, 0, 0);
     realign16(lo, hi, sh, avail, w);
 }
 
@@ -168,20 +201,21 @@ __device__ __forceinline__ uint64_t w64(const uint32_t (&w)[4], int i) {
 }
 
 // portable_hash64, hash.cpp:87-104 (read_tail :71-81)
+template <bool GEN>
 __device__ uint64_t portable_hash64(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
                                     uint64_t seed) {
     uint64_t acc = seed ^ mum((uint64_t)len ^ kP1, seed ^ kP2);
     uint32_t i = 0;
     uint32_t w[4];
     while (i + 16 <= len) {
-        load16(data, off + i, 16, w);
+        load16<GEN>(data, off + i, 16, w);
         acc = mum(w64(w, 0) ^ kP1, w64(w, 1) ^ acc);
         i += 16;
     }
     uint64_t a = 0, b = 0;
     const uint32_t rem = len - i;
     if (rem > 0) {
-        load16(data, off + i, rem, w);  // the remaining 1..15 bytes, zero padded
+        load16<GEN>(data, off + i, rem, w);  // the remaining 1..15 bytes, zero padded
         auto tail = [&](uint32_t start, uint32_t m) -> uint64_t {  // read_tail(p+start, m)
             auto byte_at = [&](uint32_t q) -> uint64_t { return (w[q >> 2] >> (8 * (q & 3))) & 0xff; };
             if (m >= 4) {
@@ -222,60 +256,52 @@ __device__ __forceinline__ void set128(uint32_t (&s)[4], uint64_t hi, uint64_t l
 // only on the seed, hash.cpp:116-119); the first round comes from the init table. The
 // zero-padded tail block (buf[15] ^= len - i) is the last iteration of the block loop, so a
 // key takes exactly ceil(len/16) absorbing rounds.
-__device__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
-                         uint64_t seed, bool wide, const DevIndex& ix, const uint4* init,
-                         uint32_t tb, uint64_t& hi, uint64_t& lo) {
+template <class L, bool GEN, bool INIT>
+__device__ __forceinline__ void aes_hash(const uint8_t* __restrict__ data, uint64_t off, uint32_t len,
+                         uint64_t seed, bool wide, const DevIndex& ix, uint32_t init_s,
+                         const L& tb, uint64_t& hi, uint64_t& lo) {
     const uint32_t k0[4] = {ix.aes_k0[0], ix.aes_k0[1], ix.aes_k0[2], ix.aes_k0[3]};
     const uint32_t k1[4] = {ix.aes_k1[0], ix.aes_k1[1], ix.aes_k1[2], ix.aes_k1[3]};
     uint32_t s[4], w[4];
-    if (len < kInitLens) {
-        const uint4 v = init[len];
-        s[0] = v.x;
-        s[1] = v.y;
-        s[2] = v.z;
-        s[3] = v.w;
+    if (INIT && len < kInitLens) {  // init: the table's shared-window address
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3])
+                     : "r"(init_s + len * 16));
     } else {
         set128(s, (uint64_t)len * kC, seed ^ (uint64_t)len);
         aesenc(s, k0, tb);
     }
-    // Block b's 16 bytes are words 4b..4b+4 of the key's 4-byte-aligned span, shifted by
-    // the key's start offset in its first word (one funnel shift per output word, no
-    // selects). Only words that hold a byte of the key are read. The blocks every active
-    // lane has in full run unmasked; the rest (each lane's zero-padded tail block, and the
-    // full blocks of lanes with more than the warp's minimum) run masked.
+    // The key's bytes arrive as aligned 16-byte granules g0..gl, prefetched one block ahead
+    // (block b needs granules b and b+1; granule b+2 is loaded while block b is hashed), and
+    // are realigned with a two-level word select and one funnel shift per word. No granule
+    // past gl is read, i.e. no access leaves the granules covering the key. Blocks below the
+    // warp's smallest full-block count skip the tail mask (a warp-uniform test); the mask is
+    // branch-free (one clamped funnel shift per word).
     const uint32_t nblk = (len + 15) >> 4;
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + off);
-    const uint32_t* wp = reinterpret_cast<const uint32_t*>(a0 & ~uintptr_t{3});
-    const uint32_t sh4 = (uint32_t)(a0 & 3), rs = sh4 * 8;
-    const uint32_t nfull = __reduce_min_sync(__activemask(), len >> 4);
-    uint32_t b = 0;
-    for (; b < nfull; b++) {
-        const uint32_t* q = wp + 4 * b;
-        const uint32_t v0 = __ldg(q), v1 = __ldg(q + 1), v2 = __ldg(q + 2), v3 = __ldg(q + 3);
-        const uint32_t v4 = sh4 ? __ldg(q + 4) : 0;
-        s[0] ^= __funnelshift_r(v0, v1, rs);
-        s[1] ^= __funnelshift_r(v1, v2, rs);
-        s[2] ^= __funnelshift_r(v2, v3, rs);
-        s[3] ^= __funnelshift_r(v3, v4, rs);
-        aesenc(s, k1, tb);
-    }
-    for (; b < nblk; b++) {
-        const uint32_t rem = len - (b << 4);  // bytes left: >= 16, or the tail's 1..15
-        const uint32_t nw = (sh4 + (rem < 16 ? rem : 16) + 3) >> 2;  // words holding key bytes
-        const uint32_t* q = wp + 4 * b;
-        uint32_t v[5];
+    const uint4* gp = reinterpret_cast<const uint4*>(a0 & ~uintptr_t{15});
+    const uint32_t sh = (uint32_t)(a0 & 15);
+    const uint32_t gl = len ? (sh + len - 1) >> 4 : 0;
+    const uint32_t nmin = __reduce_min_sync(__activemask(), len >> 4);
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    uint4 cur = nblk ? ldq<GEN>(gp) : zero;
+    uint4 nxt = gl >= 1 ? ldq<GEN>(gp + 1) : zero;
+    for (uint32_t b = 0; b < nblk; b++) {
+        const uint4 nn = b + 2 <= gl ? ldq<GEN>(gp + b + 2) : zero;  // prefetch
+        realign16(cur, nxt, sh, 16, w);
+        if (b >= nmin) {  // this lane may be in its zero-padded tail block
+            const uint32_t rem = len - (b << 4);
+            const int base = 32 - 8 * (int)rem;  // word t keeps rem - 4t bytes
 #pragma unroll
-        for (int i = 0; i < 5; i++) v[i] = (uint32_t)i < nw ? __ldg(q + i) : 0;
-        const int base = 32 - 8 * (int)rem;  // word t keeps rem - 4t bytes
-#pragma unroll
-        for (int t = 0; t < 4; t++) {
-            const uint32_t m = __funnelshift_rc(0xffffffffu, 0u, (uint32_t)max(base + 32 * t, 0));
-            w[t] = __funnelshift_r(v[t], v[t + 1], rs) & m;
+            for (int t = 0; t < 4; t++)
+                w[t] &= __funnelshift_rc(0xffffffffu, 0u, (uint32_t)max(base + 32 * t, 0));
+            if (rem < 16) w[3] ^= rem << 24;  // buf[15] ^= len - i
         }
-        if (rem < 16) w[3] ^= rem << 24;  // buf[15] ^= len - i
 #pragma unroll
         for (int c = 0; c < 4; c++) s[c] ^= w[c];
         aesenc(s, k1, tb);
+        cur = nxt;
+        nxt = nn;
     }
     aesenc(s, k0, tb);
     aesenc(s, k1, tb);
@@ -302,6 +328,115 @@ constexpr int kBytesThreads = PH_STR_THREADS;
 constexpr int kBytesWarps = kBytesThreads / 32;
 constexpr uint32_t kClasses = 8;  // block counts 0..6, and 7 for >= 7 blocks
 
+// hash_bytes (hash.cpp:159-193) of the key at data[o0, o1) with the index's string hash.
+template <bool GEN = false, bool INIT = false, class L>
+__device__ __forceinline__ void hash_key(const uint8_t* __restrict__ data, uint64_t o0,
+                                         uint64_t o1, const DevIndex& ix, uint32_t init_s,
+                                         const L& look, uint64_t& hi, uint64_t& lo) {
+    const int algo = ix.hash_algo;
+    const uint32_t len = (uint32_t)(o1 - o0);
+    if (algo == 1 || algo == 2) {
+        aes_hash<L, GEN, INIT>(data, o0, len, ix.seed, algo == 2, ix, init_s, look, hi, lo);
+    } else if (algo == 4) {
+        hi = portable_hash64<GEN>(data, o0, len, ix.seed ^ kP3);
+        lo = portable_hash64<GEN>(data, o0, len, mix64(ix.seed) + kGolden);
+    } else {
+        hi = lo = portable_hash64<GEN>(data, o0, len, ix.seed);
+    }
+}
+
+// part_and_bucket (bucket_fn.hpp:66-72) of a hashed key and its pilot gather, issued
+// without waiting (FAST: the bracketed bucket form, ph_arith.cuh).
+template <int G, bool FAST, bool HOTF = true>
+__device__ __forceinline__ uint32_t locate(const DevIndex& ix, bool valid, uint64_t hi,
+                                           uint32_t& part, uint64_t pol_keep, uint64_t pol_cold) {
+    uint64_t x;
+    part = (uint32_t)mul32x64((uint32_t)ix.P, hi, x);  // P, B < 2^32 (create)
+    const uint32_t bucket = bucket_of<G, FAST>(x, (uint32_t)ix.B, ix.opt_table);
+    if constexpr (!HOTF)  // the file's own layout (hot_b == B)
+        return valid ? ld_gather_u8(ix.pilots + ((uint64_t)part * (uint32_t)ix.B + bucket), pol_keep)
+                     : 0;
+    const bool hot = bucket < ix.hot_b;
+    return valid ? ld_gather_u8(ix.pilots + pilot_offset(ix, part, bucket),
+                                (hot || !ix.cold_evict_first) ? pol_keep : pol_cold)
+                 : 0;
+}
+
+// slot_of + remap_slot (index.hpp:91-100) from the key's part, low hash word and pilot,
+// stored to *dst; warp-collective (the rare remap decodes run convergently), `valid` masks
+// the lanes without a key.
+template <bool POW2, int MF, class OutT>
+__device__ __forceinline__ void finish(const DevIndex& ix, bool valid, uint32_t part,
+                                       uint64_t lo, uint32_t pilot, int minimal, OutT* dst) {
+    uint64_t slot = (uint64_t)part * (uint32_t)ix.S + reduce<POW2, MF>(ix, lo ^ hash_pilot(ix, pilot));
+    if (minimal) {
+        const bool need = valid && slot >= ix.n;
+        if (__any_sync(kFull, need)) {
+            // rare path: every flagged lane decodes (one convergent round per warp)
+            uint64_t v = 0;
+            if (need) v = remap_get(ix, slot - ix.n);
+            if (need) slot = v;
+        }
+    }
+    if (valid) st_stream(dst, slot);
+}
+
+template <int G, bool POW2, class OutT>
+__device__ __forceinline__ void answer_key(const DevIndex& ix, bool valid, uint64_t hi,
+                                           uint64_t lo, int minimal, OutT* dst,
+                                           uint64_t pol_keep, uint64_t pol_cold) {
+    uint32_t part;
+    const uint32_t pilot = locate<G, false>(ix, valid, hi, part, pol_keep, pol_cold);
+    finish<POW2, -1>(ix, valid, part, lo, pilot, minimal, dst);
+}
+
+// Batches of at most 32 keys (single-key index(), tiny batches): one warp, one key per lane,
+// AES T-tables read from global memory (4 KiB, L1-resident) instead of filling the 128 KiB
+// shared-memory copies, which would dominate a one-key launch.
+template <int G, bool POW2, class OutT>
+__global__ void __launch_bounds__(32) k_query_bytes_small(const DevIndex ix,
+                                                          const uint8_t* __restrict__ data,
+                                                          const uint64_t* __restrict__ offsets,
+                                                          uint64_t base_off, OutT* __restrict__ out,
+                                                          uint64_t nkeys, int minimal) {
+    __shared__ __align__(16) uint32_t tab[1024];
+    const unsigned lane = threadIdx.x;
+    const bool valid = lane < nkeys;
+    if (ix.hash_algo == 1 || ix.hash_algo == 2) stage_aes_tab(tab, ix.aes_tab);
+    __syncwarp();
+    uint64_t hi = 0, lo = 0;
+    if (valid)
+        hash_key(data, offsets[lane] - base_off, offsets[lane + 1] - base_off, ix, 0u,
+                 FlatLook{tab}, hi, lo);
+    answer_key<G, POW2>(ix, valid, hi, lo, minimal, out + lane, policy_evict_last(),
+                        policy_evict_first());
+}
+
+// index(string_view) for one key of at most kOneKeyBytes bytes (ph_gpu_index_bytes): the key
+// travels in the launch parameters, so the kernel reads nothing from the host; it is staged
+// in shared memory and hashed by lane 0.
+constexpr uint32_t kOneKeyBytes = 256;  // (launch-parameter bytes cost launch latency)
+struct OneKey {
+    uint4 bytes[kOneKeyBytes / 16];
+    uint64_t len;
+};
+template <int G, bool POW2>
+__global__ void __launch_bounds__(32) k_index_bytes_one(const DevIndex ix, const OneKey key,
+                                                        uint64_t* __restrict__ out, int minimal) {
+    __shared__ __align__(16) uint4 kb[kOneKeyBytes / 16];
+    __shared__ __align__(16) uint32_t tab[1024];
+    const unsigned lane = threadIdx.x;
+    if (ix.hash_algo == 1 || ix.hash_algo == 2) stage_aes_tab(tab, ix.aes_tab);
+    for (uint32_t i = lane; i < (uint32_t)(key.len + 15) / 16; i += 32) kb[i] = key.bytes[i];
+    __syncwarp();
+    uint64_t hi = 0, lo = 0;
+    if (lane == 0)
+        hash_key<true>(reinterpret_cast<const uint8_t*>(kb), 0, key.len, ix, 0u,
+                       FlatLook{tab}, hi, lo);
+    answer_key<G, POW2>(ix, lane == 0, hi, lo, minimal, out, policy_evict_last(),
+                        policy_evict_first());
+}
+
 // Dynamic shared memory of k_query_bytes: BytesLow from the start of the window, the AES
 // tables at shared address kTabBase (so the allocation spans kTabBase + 128 KiB minus the
 // window's start; BytesLow must end below kTabBase, checked at run time).
@@ -312,7 +447,7 @@ struct BytesLow {
 };
 constexpr size_t kBytesSmem = kTabBase + sizeof(AesTables);  // 192 KiB
 
-template <int G, bool POW2, class OutT>
+template <int G, bool POW2, class OutT, int MF, bool HOTF>
 __global__ void __launch_bounds__(kBytesThreads, 1) k_query_bytes(const DevIndex ix,
                                                      const uint8_t* __restrict__ data,
                                                      const uint64_t* __restrict__ offsets,
@@ -328,7 +463,8 @@ __global__ void __launch_bounds__(kBytesThreads, 1) k_query_bytes(const DevIndex
     const int algo = ix.hash_algo;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1;
-    const uint32_t tb = kTabBase + lane * 4;
+    const SmemLook tb{kTabBase + lane * 4};
+    const uint32_t init_s = (uint32_t)__cvta_generic_to_shared(SM.init);
     if (algo == 1 || algo == 2) {
         fill_tables(T);
         __syncthreads();
@@ -357,6 +493,14 @@ __global__ void __launch_bounds__(kBytesThreads, 1) k_query_bytes(const DevIndex
         }
         if (lane == 0 && cnt == kBatch) so[kBatch] = __ldg(offsets + base + kBatch);
         __syncwarp();
+        // The batch's key bytes are one contiguous span (~4.6 KB at config 4): touch all of
+        // its lines now (L2 prefetch), so the keys hashed later in the batch find them there.
+        {
+            const uintptr_t lo = reinterpret_cast<uintptr_t>(data + (so[0] - base_off)) & ~uintptr_t{127};
+            const uintptr_t hi = reinterpret_cast<uintptr_t>(data + (so[cnt] - base_off));
+            for (uintptr_t a = lo + lane * 128; a < hi; a += 32 * 128)
+                prefetch_l2(reinterpret_cast<const void*>(a));
+        }
         // counting sort of the batch by block count (invalid slots last)
         uint32_t cls[kBatchPer];
 #pragma unroll
@@ -382,41 +526,29 @@ __global__ void __launch_bounds__(kBytesThreads, 1) k_query_bytes(const DevIndex
             }
         }
         __syncwarp();
-        for (int q = 0; q < kBatchPer; q++) {
-            const uint32_t e = sp[q * 32 + lane];
-            const bool valid = e < cnt;
-            uint64_t hi = 0, lo = 0;
-            if (valid) {
-                const uint64_t o0 = so[e] - base_off, o1 = so[e + 1] - base_off;
-                const uint32_t len = (uint32_t)(o1 - o0);
-                if (algo == 1 || algo == 2) {
-                    aes_hash(data, o0, len, ix.seed, algo == 2, ix, SM.init, tb, hi, lo);
-                } else if (algo == 4) {
-                    hi = portable_hash64(data, o0, len, ix.seed ^ kP3);
-                    lo = portable_hash64(data, o0, len, mix64(ix.seed) + kGolden);
-                } else {
-                    hi = lo = portable_hash64(data, o0, len, ix.seed);
-                }
+        // hash the batch's keys 32 at a time; each key's pilot gather is issued as soon as its
+        // hash is known and the key is finished one round later, so the gather overlaps the
+        // next key's hashing (one copy of the hash code: the loop is not unrolled)
+        uint32_t pe = 0xffffffffu, ppart = 0, ppilot = 0;
+        uint64_t plo = 0;
+#pragma unroll 1
+        for (int q = 0; q <= kBatchPer; q++) {
+            uint32_t e = 0xffffffffu, part = 0, pilot = 0;
+            uint64_t lo = 0;
+            if (q < kBatchPer) {  // (warp-uniform)
+                e = sp[q * 32 + lane];
+                const bool valid = e < cnt;
+                uint64_t hi = 0;
+                if (valid)
+                    hash_key<false, true>(data, so[e] - base_off, so[e + 1] - base_off, ix,
+                                          init_s, tb, hi, lo);
+                pilot = locate<G, true, HOTF>(ix, valid, hi, part, pol_keep, pol_cold);
             }
-            uint64_t x;
-            const uint64_t part = mul32x64((uint32_t)ix.P, hi, x);  // P, B < 2^32 (create)
-            const uint64_t bucket = bucket_of<G>(x, (uint32_t)ix.B, ix.opt_table);
-            const bool hot = bucket < ix.hot_b;
-            const uint32_t pilot =
-                valid ? ld_gather_u8(ix.pilots + pilot_offset(ix, part, bucket),
-                                     (hot || !ix.cold_evict_first) ? pol_keep : pol_cold)
-                      : 0;
-            uint64_t slot = part * ix.S + reduce<POW2>(ix, lo ^ hash_pilot(ix, pilot));
-            if (minimal) {
-                const bool need = valid && slot >= ix.n;
-                if (__any_sync(kFull, need)) {
-                    // rare path: every flagged lane decodes (one convergent round per warp)
-                    uint64_t v = 0;
-                    if (need) v = remap_get(ix, slot - ix.n);
-                    if (need) slot = v;
-                }
-            }
-            if (valid) st_stream(out + base + e, slot);
+            if (q > 0) finish<POW2, MF>(ix, pe < cnt, ppart, plo, ppilot, minimal, out + base + pe);
+            pe = e;
+            ppart = part;
+            ppilot = pilot;
+            plo = lo;
         }
         __syncwarp();  // s_off / s_perm are rewritten by the next batch
     }
@@ -425,7 +557,20 @@ __global__ void __launch_bounds__(kBytesThreads, 1) k_query_bytes(const DevIndex
 template <int G, bool POW2, class OutT>
 static cudaError_t launch_b(const DevIndex& ix, const uint8_t* d, const uint64_t* o,
                             uint64_t bo, void* out, uint64_t n, int minimal, cudaStream_t s, int sms) {
-    auto kern = k_query_bytes<G, POW2, OutT>;
+    if (n <= 32) {
+        const cudaError_t e = launch_ex(ix, k_query_bytes_small<G, POW2, OutT>, 1, 32, s, ix, d, o,
+                                        bo, static_cast<OutT*>(out), n, minimal);
+        note_launch();
+        return e;
+    }
+    const bool hotf = ix.hot_b < ix.B;
+    void (*kern)(const DevIndex, const uint8_t*, const uint64_t*, uint64_t, OutT*, uint64_t, int);
+    if constexpr (POW2)
+        kern = hotf ? k_query_bytes<G, true, OutT, 0, true> : k_query_bytes<G, true, OutT, 0, false>;
+    else if (ix.mod_fast_ok)
+        kern = hotf ? k_query_bytes<G, false, OutT, 1, true> : k_query_bytes<G, false, OutT, 1, false>;
+    else
+        kern = hotf ? k_query_bytes<G, false, OutT, 0, true> : k_query_bytes<G, false, OutT, 0, false>;
     constexpr size_t smem = kBytesSmem;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int bps = 0;
@@ -459,6 +604,45 @@ static cudaError_t launch_bw(const DevIndex& ix, int g, bool pow2, const uint8_t
     }
 #undef PH_CASE
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_index_bytes_one(const DevIndex& ix, int gamma_kind, bool pow2,
+                                   const uint8_t* key, uint32_t len, uint64_t* out, int minimal,
+                                   cudaStream_t s) {
+    if (len > kOneKeyBytes) return cudaErrorInvalidValue;
+    OneKey k{};
+    memcpy(k.bytes, key, len);
+    k.len = len;
+#define PH_CASE(G)                                                                            \
+    case G:                                                                                   \
+        if (pow2) k_index_bytes_one<G, true><<<1, 32, 0, s>>>(ix, k, out, minimal);          \
+        else k_index_bytes_one<G, false><<<1, 32, 0, s>>>(ix, k, out, minimal);              \
+        break;
+    switch (gamma_kind) {
+        PH_CASE(0)
+        PH_CASE(1)
+        PH_CASE(2)
+        PH_CASE(3)
+        PH_CASE(4)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef PH_CASE
+    note_launch();
+    return cudaGetLastError();
+}
+
+// T0..T3 once in global memory (DevIndex::aes_tab), filled at index creation.
+__global__ void k_fill_aes_tab(uint32_t* tab) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // 1024 entries
+    if (e < 1024) {
+        const uint32_t v = t0_entry(e & 255);
+        tab[e] = __funnelshift_l(v, v, 8 * (e >> 8));
+    }
+}
+cudaError_t launch_fill_aes_tab(uint32_t* tab, cudaStream_t s) {
+    k_fill_aes_tab<<<4, 256, 0, s>>>(tab);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_query_bytes(const DevIndex& ix, int gamma_kind, bool pow2,

@@ -64,7 +64,7 @@ _L.ph_gpu_query_kmers.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C
 _L.ph_gpu_index_stream_kmers.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p,
                                          C.c_int, C.c_int]
 _L.ph_gpu_index_u64.argtypes = [C.c_void_p, C.c_uint64, C.c_int, u64p]
-_L.ph_gpu_index_bytes.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, u64p]
+_L.ph_gpu_index_bytes.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t, C.c_int, u64p]
 _L.ph_gpu_launch_count.restype = C.c_uint64
 _L.ph_gpu_index_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
 _L.ph_gpu_verify_bijection.argtypes = [C.c_void_p, C.c_size_t, C.c_int, C.c_uint64, C.c_int,
@@ -73,8 +73,11 @@ _L.ph_gpu_set_launch.argtypes = [C.c_int, C.c_int]
 _L.ph_gpu_set_partition.argtypes = [C.c_int]
 _L.ph_gpu_set_regime.argtypes = [C.c_int]
 _L.ph_gpu_index_set_l2_policy.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
-_L.ph_gpu_index_set_scratch_limit.argtypes = [C.c_void_p, C.c_uint64]
-_L.ph_gpu_gather_replay_u64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+try:  # (absent from tuning builds of older sources, tools/variant_ab.py)
+    _L.ph_gpu_index_set_scratch_limit.argtypes = [C.c_void_p, C.c_uint64]
+    _L.ph_gpu_gather_replay_u64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+except AttributeError:
+    pass
 
 # status codes (ph_gpu.h)
 OK, E_INVALID, E_FORMAT, E_CUDA, E_KEYKIND, E_NOMEM, E_UNSUPPORTED = range(7)
@@ -325,8 +328,7 @@ class PtrHashIndex:
         out = C.c_uint64()
         if isinstance(key, (bytes, bytearray, str)):
             b = key.encode() if isinstance(key, str) else bytes(key)
-            arr = (C.c_uint8 * max(1, len(b))).from_buffer_copy(b if b else b"\0")
-            _check(_L.ph_gpu_index_bytes(self._h, arr, len(b), int(minimal), C.byref(out)))
+            _check(_L.ph_gpu_index_bytes(self._h, b, len(b), int(minimal), C.byref(out)))
         else:
             _check(_L.ph_gpu_index_u64(self._h, int(key) & (2**64 - 1), int(minimal),
                                        C.byref(out)))

@@ -159,6 +159,11 @@ int ph_gpu_verify_bijection(const void* d_out, size_t count, int out_width, uint
 int ph_gpu_gather_replay_u64(const ph_gpu_index* index, const uint64_t* d_keys, size_t n,
                              ph_gpu_stream_t stream);
 
+/* Checked builds only (-DPH_CHECKS; tools/checked_run.py): device-side bounds violations of
+ * the partitioned path's staging, bulk copies and scatters plus scratch canary damage, since
+ * the last call. PH_E_UNSUPPORTED in normal builds. */
+int ph_gpu_check_errors(uint64_t* count, uint64_t* first_line);
+
 /* ---- introspection ---- */
 /* Number of query-kernel launches this process made through this library. */
 uint64_t ph_gpu_launch_count(void);

@@ -517,6 +517,12 @@ int ph_gpu_pass_times(double* ms_sums3, int* calls) {
     return phg::pass_times(ms_sums3, calls) == 0 ? PH_OK
                                                  : fail(PH_E_CUDA, "pass timing events failed");
 }
+int ph_gpu_check_errors(uint64_t* count, uint64_t* first_line) {
+    if (!count || !first_line) return fail(PH_E_INVALID, "null argument");
+    const int r = phg::check_errors(count, first_line);
+    if (r == -1) return fail(PH_E_UNSUPPORTED, "not a checked build (-DPH_CHECKS)");
+    return r == 0 ? PH_OK : fail(PH_E_CUDA, "reading the check counters failed");
+}
 int ph_gpu_set_partition(int mode) {
     if (mode < 0 || mode > 2) return fail(PH_E_INVALID, "partition mode must be 0, 1 or 2");
     g_partition.store(mode);
@@ -734,6 +740,8 @@ int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, v
     if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
     if (n == 0) return PH_OK;
     if (!d_keys || !d_out) return fail(PH_E_INVALID, "null key or output pointer");
+    if ((reinterpret_cast<uintptr_t>(d_keys) & 7) || (reinterpret_cast<uintptr_t>(d_out) & (out_width - 1)))
+        return fail(PH_E_INVALID, "keys must be 8-byte aligned and out aligned to out_width");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     if (const uint32_t G = partition_groups(ix, n, out_width)) {
@@ -758,6 +766,8 @@ int ph_gpu_query_bytes(const ph_gpu_index* ix, const uint8_t* d_bytes, const uin
     if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
     if (n == 0) return PH_OK;
     if (!d_bytes || !d_offsets || !d_out) return fail(PH_E_INVALID, "null pointer argument");
+    if ((reinterpret_cast<uintptr_t>(d_offsets) & 7) || (reinterpret_cast<uintptr_t>(d_out) & (out_width - 1)))
+        return fail(PH_E_INVALID, "offsets must be 8-byte aligned and out aligned to out_width");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     cudaError_t e = phg::launch_query_bytes(ix->dev, ix->info.bucket_fn, ix->info.pow2, d_bytes,
@@ -1052,6 +1062,8 @@ int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n
     if (int rc = check_u32_range(ix, out_width, minimal)) return rc;
     if (n_bases < (uint64_t)k) return PH_OK;
     if (!d_seq || !d_out) return fail(PH_E_INVALID, "null sequence or output pointer");
+    if ((reinterpret_cast<uintptr_t>(d_seq) & 7) || (reinterpret_cast<uintptr_t>(d_out) & (out_width - 1)))
+        return fail(PH_E_INVALID, "seq must be 8-byte aligned and out aligned to out_width");
     DeviceGuard g(ix->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     const uint64_t nwin = n_bases - (uint64_t)k + 1;

@@ -84,6 +84,9 @@ cudaError_t launch_query_partitioned(const DevIndex& ix, int gamma_kind, bool po
                                      int minimal, uint32_t G, void* scratch, cudaStream_t s,
                                      int sms);
 
+// Device-side check violations of a -DPH_CHECKS build (ph_partition.cu); -1 otherwise.
+int check_errors(uint64_t* count, uint64_t* line);
+
 // Per-pass event timing of the partitioned path (A, B, C), summed over the timed calls.
 void set_pass_timing(bool on);
 int pass_times(double* ms_sums, int* calls);

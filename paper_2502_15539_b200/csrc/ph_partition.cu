@@ -38,6 +38,29 @@
 
 namespace phg {
 
+// Checked builds (-DPH_CHECKS, tools/checked_run.py; compute-sanitizer is closed on this GPU
+// pool): every shared-memory staging index, bulk-copy range and scatter position of passes
+// A-C is bounds-checked on the device, and a canary band after the scratch is verified.
+// Violations are counted (no trap), read back with ph_gpu_check_errors.
+#ifdef PH_CHECKS
+struct ChkBounds {
+    uint64_t nent;       // entries in bins / bpos / slots
+    uint64_t n;          // keys (windows)
+    uint64_t in_words;   // words readable at `keys` (u64 keys: n; k-mers: sequence words)
+    uint64_t ntiles;
+};
+__device__ ChkBounds g_chk_b;
+__device__ unsigned long long g_chk[2];  // [0] violations, [1] source line of the first
+#define PH_CHECK(c)                                                                   \
+    do {                                                                              \
+        if (!(c) && atomicAdd(&g_chk[0], 1ull) == 0) g_chk[1] = __LINE__;            \
+    } while (0)
+#else
+#define PH_CHECK(c) \
+    do {            \
+    } while (0)
+#endif
+
 #ifndef PH_TILE_KEYS
 #define PH_TILE_KEYS 4096
 #endif
@@ -320,6 +343,9 @@ __global__ void __launch_bounds__(THREADS, SRC == 1 ? PH_BIN_KMER_CTAS : 2) k_bi
     __syncthreads();
     auto issue = [&](uint64_t t, int b) {  // thread 0: bulk-load tile t's input into buffer b
         constexpr uint32_t bytes = SRC == 1 ? kSeqWords * 8 : kTileKeys * 8;
+#ifdef PH_CHECKS
+        PH_CHECK(t * (SRC == 1 ? kTileKeys / 32 : kTileKeys) + bytes / 8 <= g_chk_b.in_words);
+#endif
         mbar_expect_tx(&bar[b], bytes);
         bulk_g2s(in + b * IW, keys + t * (SRC == 1 ? kTileKeys / 32 : kTileKeys), bytes,
                  &bar[b], pol);
@@ -405,6 +431,7 @@ __global__ void __launch_bounds__(THREADS, SRC == 1 ? PH_BIN_KMER_CTAS : 2) k_bi
             const uint32_t pos = (uint32_t)j * THREADS + tid;
             if (pos < valid) {
                 const uint32_t e = lb8[gr[j] >> 16] + (gr[j] & 0xffffu);
+                PH_CHECK(e < kBinTmaStage && (gr[j] >> 16) < G);
                 sk[e] = k[j];
                 sp[e] = (uint16_t)pos;
             }
@@ -424,6 +451,10 @@ __global__ void __launch_bounds__(THREADS, SRC == 1 ? PH_BIN_KMER_CTAS : 2) k_bi
         if (warp == 0) {  // lane issues the bulk stores of its group's run
             if (lane < G && rc[lane]) {
                 const uint32_t c8 = (rc[lane] + 7) & ~7u, l = lb8[lane];
+#ifdef PH_CHECKS
+                PH_CHECK(l + c8 <= kBinTmaStage && roff[lane] + c8 <= g_chk_b.nent &&
+                         (roff[lane] & 7) == 0);
+#endif
                 bulk_s2g(bins + roff[lane], sk + l, c8 * 8, pol);
                 bulk_s2g(bpos + roff[lane], sp + l, c8 * 2, pol);
             }
@@ -493,6 +524,10 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
         OutT* sv;
         uint16_t* pv;
         bufs(b, sv, pv);
+#ifdef PH_CHECKS
+        PH_CHECK(x + p0 + p1 <= kStageEntries && total <= kStageEntries);
+        PH_CHECK((!p0 || m.o0 + p0 <= g_chk_b.nent) && (!p1 || m.o1 + p1 <= g_chk_b.nent));
+#endif
         if (p0) {
             bulk_g2s(sv + x, slots + m.o0, p0 * (uint32_t)sizeof(OutT), &bar[b], pol);
             bulk_g2s(pv + x, bpos + m.o0, p0 * 2, &bar[b], pol);
@@ -531,6 +566,7 @@ __global__ void __launch_bounds__(kBinThreads) k_unbin_tma(
 #pragma unroll 4
         for (uint32_t e = tid; e < total; e += kBinThreads) {
             const uint16_t p = pv[e];
+            PH_CHECK(p == kPadPos || p < valid);
             if (p != kPadPos) stage[p] = sv[e];
         }
         fence_async_smem();
@@ -600,6 +636,9 @@ __global__ void __launch_bounds__(kQThreads, PH_QB_MINB) k_query_regions(
         while (c >= cstart[r + 1]) r++;
         const uint64_t e0 = (uint64_t)r * cap + (c - cstart[r]) * kQChunk;
         const uint64_t end = rend[r];  // region lengths are multiples of 8 entries
+#ifdef PH_CHECKS
+        PH_CHECK(end <= g_chk_b.nent && (end & 7) == 0 && e0 < end);
+#endif
         uint64_t h[kQPer];
 #pragma unroll
         for (int q = 0; q < kQPer / 2; q++) {
@@ -677,6 +716,12 @@ static cudaError_t launch_regions(const DevIndex& ix, int gamma_kind, bool pow2,
 }
 
 // ---------------------------------------------------------------------------
+#ifdef PH_CHECKS
+constexpr uint64_t kCanaryBytes = 4096;
+__global__ void k_canary_check(const uint32_t* p, uint32_t words) {
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) PH_CHECK(p[i] == 0xA5A5A5A5u);
+}
+#endif
 namespace {
 struct Layout {
     uint64_t cap, ntiles, nent;
@@ -703,6 +748,9 @@ Layout layout(uint64_t n, uint32_t G, int out_width) {
     o += al(L.nent * 2);
     L.o_slots = o;
     o += al(L.nent * (uint64_t)out_width);
+#ifdef PH_CHECKS
+    o += kCanaryBytes;  // canary band after the scratch (checked builds)
+#endif
     L.total = o;
     return L;
 }
@@ -782,6 +830,13 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
     pt_record(0, s);
     cudaError_t e = cudaMemsetAsync(ctrl, 0, kCtrlWords * 8, s);
     if (e != cudaSuccess) return e;
+#ifdef PH_CHECKS
+    {
+        const ChkBounds cb{L.nent, n, src_kind == 1 ? seq_words : n, L.ntiles};
+        cudaMemcpyToSymbolAsync(g_chk_b, &cb, sizeof(cb), 0, cudaMemcpyHostToDevice, s);
+        cudaMemsetAsync(base + L.total - kCanaryBytes, 0xA5, kCanaryBytes, s);
+    }
+#endif
     // A: bin the keys by group
     const size_t smem_a = kTileKeys * (8 + 4);
     // (per device and cheap: set on every call)
@@ -842,7 +897,28 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
             n, G, runoff, runcnt, bpos, static_cast<const uint64_t*>(slots), static_cast<uint64_t*>(out));
     note_launch();
     pt_record(3, s);
+#ifdef PH_CHECKS
+    k_canary_check<<<1, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(base + L.total - kCanaryBytes),
+                                     (uint32_t)(kCanaryBytes / 4));
+#endif
     return cudaGetLastError();
+}
+
+// Violations counted by a checked build since the last call (and the source line of the
+// first); -1 in normal builds.
+int check_errors(uint64_t* count, uint64_t* line) {
+#ifdef PH_CHECKS
+    unsigned long long h[2] = {0, 0};
+    if (cudaMemcpyFromSymbol(h, g_chk, sizeof(h)) != cudaSuccess) return -2;
+    const unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_chk, z, sizeof(z));
+    *count = h[0];
+    *line = h[1];
+    return 0;
+#else
+    *count = *line = 0;
+    return -1;
+#endif
 }
 
 }  // namespace phg

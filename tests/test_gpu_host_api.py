@@ -137,3 +137,23 @@ def test_wrapper_checks_with_device_tensors(ph, ref):
     out = idx.query(d_keys, stream=s)  # torch.cuda.Stream objects are accepted
     s.synchronize()
     assert out.numel() == keys.size
+
+
+def test_misaligned_device_pointers_are_rejected(ph, ref):
+    """A u64 key array not 8-byte aligned (or an output not aligned to its width) is an
+    argument error, not a device fault that would poison the context."""
+    from oracle.bindings import corpus_u64_np
+    keys = corpus_u64_np(0, 20_000, 4)
+    idx = ph.PtrHashIndex(ref.build_u64(keys, ref.params("default", lambda_=(30, 10))))
+    buf = torch.zeros(keys.size * 8 + 16, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(keys.size + 4, dtype=torch.int32, device="cuda")
+    rc = ph._L.ph_gpu_query_u64(idx._h, C.c_void_p(buf.data_ptr() + 3), keys.size,
+                                C.c_void_p(out.data_ptr()), 4, 1, None)
+    assert rc == ph.E_INVALID
+    rc = ph._L.ph_gpu_query_u64(idx._h, C.c_void_p(buf.data_ptr()), keys.size,
+                                C.c_void_p(out.data_ptr() + 2), 4, 1, None)
+    assert rc == ph.E_INVALID
+    rc = ph._L.ph_gpu_query_u64(idx._h, C.c_void_p(buf.data_ptr() + 8), keys.size,
+                                C.c_void_p(out.data_ptr() + 4), 4, 1, None)
+    assert rc == ph.OK  # 8-B / 4-B aligned (not 16-B): served
+    torch.cuda.synchronize()

@@ -317,9 +317,7 @@ __global__ void __launch_bounds__(THREADS, SRC == 1 ? PH_BIN_KMER_CTAS : 2) k_bi
     uint16_t* sp = reinterpret_cast<uint16_t*>(sk + kBinTmaStage);
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t cnt[2][kTmaGroups];
-    __shared__ uint32_t lb8[kTmaGroups];
-    __shared__ uint32_t rc[kTmaGroups];
-    __shared__ uint64_t roff[kTmaGroups];
+    __shared__ uint32_t lb8[kTmaGroups];  // staging bases (the k-mer variant's shared scan)
     constexpr int PER = kTileKeys / THREADS;
     const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
@@ -396,25 +394,33 @@ __global__ void __launch_bounds__(THREADS, SRC == 1 ? PH_BIN_KMER_CTAS : 2) k_bi
             }
         }
         uint32_t* c_ = cnt[b];
+        // TWO: two CTA barriers per tile (u64 keys). Warp 0 waits for the previous tile's run
+        // stores to finish reading the staging buffer while the other warps rank, and every
+        // warp scans the group counts itself. Otherwise (k-mers, whose ranking is too short
+        // to hide that wait) warp 0 waits after barrier #1 and publishes the scan behind a
+        // second barrier (u64: 3.18 -> 3.07 ms at config 3; k-mers: 3.58 vs 3.79 ms).
+        constexpr bool TWO = SRC == 0;
+        if (TWO && warp == 0) bulk_wait_read();
         uint32_t gr[PER];  // group << 16 | rank
 #pragma unroll
         for (int j = 0; j < PER; j++) {
+            gr[j] = 0;
             if ((uint32_t)j * THREADS + tid < valid) {
                 const uint32_t g = group_of(k[j], seed, G);
                 gr[j] = g << 16 | atomicAdd(&c_[g], 1u);
             }
         }
-        __syncthreads();  // #1: buffer b consumed, counts final
+        __syncthreads();  // #1: buffer b consumed, counts final (TWO: staging free)
         if (tid == 0 && bulk(t + 2 * (uint64_t)gridDim.x)) issue(t + 2 * (uint64_t)gridDim.x, b);
         if (tid < kTmaGroups) cnt[b ^ 1][tid] = 0;  // next tile's counters
-        // warp 0 (lane = group): the run reservation is issued first (its latency overlaps
-        // the scan, barrier #2 and the staging)
-        uint32_t c = 0;
+        // lane g: group g's count; warp 0 reserves the runs (one global atomicAdd per group,
+        // its latency overlapping the scan and the staging)
+        uint32_t c = 0, lb = 0;
         unsigned long long a = 0;
-        if (warp == 0) {
+        if (TWO || warp == 0) {
             c = lane < G ? c_[lane] : 0;
-            if (c) a = atomicAdd(ctrl + lane, (unsigned long long)((c + 7) & ~7u));
-            bulk_wait_read();  // the previous tile's run stores have read the staging buffer
+            if (warp == 0 && c) a = atomicAdd(ctrl + lane, (unsigned long long)((c + 7) & ~7u));
+            if (!TWO) bulk_wait_read();  // the previous tile's run stores have read the staging
             const uint32_t p8 = (c + 7) & ~7u;
             uint32_t x = p8;
 #pragma unroll
@@ -422,41 +428,39 @@ __global__ void __launch_bounds__(THREADS, SRC == 1 ? PH_BIN_KMER_CTAS : 2) k_bi
                 const uint32_t y = __shfl_up_sync(kFull, x, o);
                 if (lane >= (unsigned)o) x += y;
             }
-            lb8[lane] = x - p8;
-            rc[lane] = c;
+            lb = x - p8;  // this lane's group's staging base
+            if (!TWO) lb8[lane] = lb;
         }
-        __syncthreads();  // #2: staging free, lb8 final
+        if (!TWO) __syncthreads();  // #2: staging free, lb8 final
 #pragma unroll
         for (int j = 0; j < PER; j++) {
             const uint32_t pos = (uint32_t)j * THREADS + tid;
+            const uint32_t base = TWO ? __shfl_sync(kFull, lb, gr[j] >> 16) : lb8[gr[j] >> 16];
+            const uint32_t e = base + (gr[j] & 0xffffu);
             if (pos < valid) {
-                const uint32_t e = lb8[gr[j] >> 16] + (gr[j] & 0xffffu);
                 PH_CHECK(e < kBinTmaStage && (gr[j] >> 16) < G);
                 sk[e] = k[j];
                 sp[e] = (uint16_t)pos;
             }
         }
+        uint64_t off = 0;
         if (warp == 0 && lane < G) {  // consume the reservation (spill if the region is full)
             const unsigned long long c8 = (c + 7u) & ~7u;
-            for (uint32_t i = c; i < c8; i++) sp[lb8[lane] + i] = kPadPos;  // padding entries
-            const uint64_t off = !c ? 0
-                                 : a + c8 <= cap ? lane * cap + a
-                                                 : G * cap + atomicAdd(ctrl + kCtrlSpill, c8);
-            roff[lane] = off;
+            for (uint32_t i = c; i < c8; i++) sp[lb + i] = kPadPos;  // padding entries
+            off = !c ? 0 : a + c8 <= cap ? lane * cap + a : G * cap + atomicAdd(ctrl + kCtrlSpill, c8);
             runoff[t * G + lane] = off;
             runcnt[t * G + lane] = (uint16_t)c;
         }
         fence_async_smem();
-        __syncthreads();  // #3: staged; run offsets known
+        __syncthreads();  // staged; run offsets known
         if (warp == 0) {  // lane issues the bulk stores of its group's run
-            if (lane < G && rc[lane]) {
-                const uint32_t c8 = (rc[lane] + 7) & ~7u, l = lb8[lane];
+            const uint32_t p8 = (c + 7) & ~7u;
+            if (lane < G && c) {
 #ifdef PH_CHECKS
-                PH_CHECK(l + c8 <= kBinTmaStage && roff[lane] + c8 <= g_chk_b.nent &&
-                         (roff[lane] & 7) == 0);
+                PH_CHECK(lb + p8 <= kBinTmaStage && off + p8 <= g_chk_b.nent && (off & 7) == 0);
 #endif
-                bulk_s2g(bins + roff[lane], sk + l, c8 * 8, pol);
-                bulk_s2g(bpos + roff[lane], sp + l, c8 * 2, pol);
+                bulk_s2g(bins + off, sk + lb, p8 * 8, pol);
+                bulk_s2g(bpos + off, sp + lb, p8 * 2, pol);
             }
             bulk_commit();
         }
@@ -599,6 +603,9 @@ constexpr uint32_t kQChunk = kQThreads * kQPer;       // 2048 entries per chunk
 #ifndef PH_QB_MINB
 #define PH_QB_MINB 4
 #endif
+#ifndef PH_QB_SEPARATE
+#define PH_QB_SEPARATE 1  // all buckets first, then the gathers back to back (5.10 vs 5.38 ms interleaved)
+#endif
 #ifndef PH_QB_CLAIM
 #define PH_QB_CLAIM 8  // chunks per claim, one CTA barrier per claim (1, 2, 4, 8, 16, 32 swept: 8-16 best, ~1 %)
 #endif
@@ -656,7 +663,15 @@ __global__ void __launch_bounds__(kQThreads, PH_QB_MINB) k_query_regions(
             uint64_t x;
             part[j] = (uint32_t)mul32x64(P32, h[j], x);  // part_and_bucket, bucket_fn.hpp:66-72
             const uint32_t bucket = bucket_of<G>(x, B32, ix.opt_table);
+#if PH_QB_SEPARATE
+            pilot[j] = bucket;
+        }
+#pragma unroll
+        for (int j = 0; j < kQPer; j++) {  // the gathers back to back (pilot[j] = bucket)
+            pilot[j] = ld_gather_u8(ix.pilots + ((uint64_t)part[j] * B32 + pilot[j]), pol_keep);
+#else
             pilot[j] = ld_gather_u8(ix.pilots + ((uint64_t)part[j] * B32 + bucket), pol_keep);
+#endif
         }
         uint64_t slot[kQPer];
         bool need[kQPer];

@@ -176,9 +176,11 @@ def ref_params(ref):
     return ref.params("default", lambda_=(30, 10))
 
 
-def build_index_bytes(n: int, dist: Dist, gen_keys, build=None, tag="u64") -> bytes:
+def build_index_bytes(n: int, dist: Dist, gen_keys, build=None, tag="u64", after=None) -> bytes:
     """Reference-built PTRH bytes; for N>1 rank 0 builds and shares through /dev/shm.
-    gen_keys(n) -> u64 keys for the reference u64 builder, or build() -> PTRH bytes."""
+    gen_keys(n) -> u64 keys for the reference u64 builder, or build() -> PTRH bytes.
+    after(keys, ptrh, ref_seconds, ref_threads) runs on rank 0 once the reference build is done
+    (the construction comparison)."""
     from oracle.bindings import Ref
     tag = hashlib.sha1(f"{tag}-{n}-{GEN_SEED}-default-l30".encode()).hexdigest()[:12]
     shm = f"/dev/shm/ph_bench_{tag}_{os.getpid() if dist.world == 1 else 'job'}.ptrh"
@@ -194,6 +196,8 @@ def build_index_bytes(n: int, dist: Dist, gen_keys, build=None, tag="u64") -> by
                 f"reference builder ({ref.hw_threads()} threads)...")
             t = time.time()
             ptrh = ref.build_u64(keys, ref_params(ref), threads=0)
+            if after is not None:
+                after(keys, ptrh, time.time() - t, ref.hw_threads())
             del keys
         log(f"[fixture] reference build {time.time() - t:.1f}s, PTRH {len(ptrh) / 1e6:.1f} MB")
         if dist.world > 1:
@@ -277,7 +281,37 @@ class U64Work:
                 keys[s:s + m] = buf[:m].cpu().numpy().view(np.uint64)
             return keys
 
-        self.ptrh = build_index_bytes(n, dist, gen_keys_gpu)
+        self.construction = None
+
+        def compare_build(keys, ptrh, ref_s, ref_threads):
+            """Construction (off the query path): the same keys and parameters
+            through ph_gpu_build_u64 (hash + sort on the GPU, pilot search on the host cores,
+            fed part by part from the device), timed by wall clock like the reference build,
+            and its PTRH bytes compared with the reference's."""
+            if not args.construction or dist.world > 1:
+                return
+            gp = ph_gpu.build_params("default", lambda_=(30, 10))
+            t = time.time()
+            ours, st = ph_gpu.build_u64(keys, gp, threads=0, device=dist.local, stats=True)
+            ours_s = time.time() - t
+            same = ours == ptrh
+            log(f"[construction] reference {ref_s:.1f}s, ours {ours_s:.1f}s "
+                f"(prepare {st['prepare_ms']:.0f} ms, search {st['search_ms']:.0f} ms), "
+                f"PTRH identical: {same}")
+            if not same:
+                raise SystemExit("construction: ph_gpu_build_u64 bytes differ from the reference's")
+            self.construction = {
+                "what": "build(keys) + serialize() of this config's index from host-resident keys: "
+                        "the reference's build() on all host threads vs ph_gpu_build_u64 "
+                        "(hash + MSD radix sort + part offsets on the GPU, pilot search on all "
+                        "host threads); wall clock, one run each",
+                "n": int(keys.size), "reference_s": round(ref_s, 3), "ours_s": round(ours_s, 3),
+                "speedup": round(ref_s / ours_s, 3), "host_threads": int(ref_threads),
+                "identical_ptrh": same, "attempts": st["attempts"],
+                "stages_ms": {k: round(st[k], 1) for k in
+                              ("upload_ms", "prepare_ms", "search_ms", "remap_ms", "total_ms")}}
+
+        self.ptrh = build_index_bytes(n, dist, gen_keys_gpu, after=compare_build)
         self.idx = ph_gpu.PtrHashIndex(self.ptrh, device=dist.local)
         if cfg.get("layout") == "file":
             # file-order pilots without a persisting window: device-resident batches of
@@ -748,6 +782,7 @@ def run_ours(args, cfg):
             "gather_buffer_bytes": int(info.pilot_bytes)},
         "replay": replay,
         "partition_passes": pass_block,
+        "construction": getattr(W, "construction", None),
         "gate": gate,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
@@ -984,6 +1019,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=100_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--no-construction", dest="construction", action="store_false",
+                    help="skip the construction comparison (ph_gpu_build_u64 vs the reference)")
     ap.add_argument("--no-secondary", dest="secondary_configs", action="store_false",
                     help="do not run configs 4 and 5 after the main config (N=1)")
     ap.add_argument("--layout", default="", choices=["", "file", "hot", "default"],

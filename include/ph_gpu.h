@@ -36,7 +36,9 @@ enum ph_gpu_status {
     PH_E_CUDA = 3,     /* CUDA runtime error (no device, launch failure, ...) */
     PH_E_KEYKIND = 4,  /* u64 query on a string index or vice versa (index.hpp:18-21) */
     PH_E_NOMEM = 5,    /* device or pinned-host allocation failed */
-    PH_E_UNSUPPORTED = 6 /* shape outside what the GPU path supports */
+    PH_E_UNSUPPORTED = 6, /* shape outside what the GPU path supports */
+    PH_E_DUPLICATE = 7,   /* build: duplicate keys (BuildError::kDuplicateKeys, build.hpp:48-61) */
+    PH_E_BUILD_FAILED = 8 /* build: every seed attempt failed (BuildError::kFailed) */
 };
 
 /* Output element width for bulk queries: u32 (all configs, n <= 2^32) or u64
@@ -137,6 +139,63 @@ int ph_gpu_index_bytes(const ph_gpu_index* index, const uint8_t* key, size_t len
 int ph_gpu_build_prepare_u64(const uint64_t* d_keys, size_t n, uint64_t parts,
                              uint64_t slots_per_part, uint64_t seed, int device,
                              uint64_t* d_hashes, uint64_t* d_offsets, int* status);
+
+/* ---- construction: the reference's u64 build with its front on the GPU ---- */
+/* BuildParams (shape.hpp:46-56). parts/slots_per_part/buckets_per_part all 0: compute_shape
+ * (shape.cpp:99-145); all set: build_with_shape (construction.cpp:145-152). */
+typedef struct ph_build_params {
+    uint32_t alpha_num, alpha_den;   /* load factor in (0, 1] */
+    uint32_t lambda_num, lambda_den; /* expected bucket size, >= 1 */
+    uint8_t bucket_fn;               /* shape.hpp:23-29 */
+    uint8_t remap_kind;              /* shape.hpp:31-35 */
+    uint8_t reduce_kind;             /* reduce.hpp:11-20 */
+    uint8_t reserved;
+    uint32_t max_seed_retries;
+    uint64_t seed;
+    uint64_t parts, slots_per_part, buckets_per_part;
+} ph_build_params;
+
+/* BuildStats (build.hpp:10-45) plus the wall time of each stage. */
+typedef struct ph_build_stats {
+    uint64_t n, parts, slots_per_part, buckets_per_part;
+    uint64_t seed;                       /* of the successful attempt */
+    uint32_t attempts;
+    uint8_t remap_kind;                  /* actual, after any CacheLineEF fallback */
+    uint8_t remap_fell_back;
+    uint8_t reserved[2];
+    uint64_t total_evictions;
+    uint64_t evictions_by_percentile[100];
+    uint64_t pilot_bytes, remap_payload_bytes;
+    double upload_ms;   /* host keys -> device */
+    double prepare_ms;  /* GPU: hash + sort + part offsets, all attempts */
+    double search_ms;   /* pilot search over all parts (overlapping the hash transfer) */
+    double remap_ms;    /* remap table + serialization */
+    double total_ms;
+} ph_build_stats;
+
+/* preset() (shape.cpp:65-84): "fast", "default", "compact". */
+int ph_build_preset(const char* name, ph_build_params* out);
+/* compute_shape (shape.cpp:99-145). */
+int ph_build_compute_shape(uint64_t n, const ph_build_params* params, uint64_t* parts,
+                           uint64_t* slots_per_part, uint64_t* buckets_per_part);
+/* build(span<const uint64_t>, params, threads, stats) + serialize() (construction.cpp:139-143,
+ * serde.cpp:142-170): the PTRH v1 bytes of the index over the distinct keys keys[0..n), which
+ * may be host or device memory. Each attempt hashes and sorts on `device`
+ * (ph_gpu_build_prepare_u64) and runs the per-part pilot search on `threads` host threads
+ * (0 = all), fed part by part from the device. The bytes equal the reference's for the same
+ * keys and parameters. *ptrh is malloc'ed: release it with ph_free. Errors: PH_E_INVALID
+ * (bad parameters or shape, empty key set), PH_E_DUPLICATE, PH_E_BUILD_FAILED, PH_E_CUDA,
+ * PH_E_NOMEM. */
+int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* params,
+                     unsigned threads, int device, uint8_t** ptrh, size_t* len,
+                     ph_build_stats* stats);
+/* The host stage of one attempt under `seed` (no GPU): hashes[0..n) are the attempt's sorted
+ * hashes in part-major order and offsets[parts+1] the part boundaries (what
+ * ph_gpu_build_prepare_u64 returns). PH_E_BUILD_FAILED if a part cannot be placed. */
+int ph_build_from_sorted_u64(const uint64_t* hashes, const uint64_t* offsets, size_t n,
+                             const ph_build_params* params, uint64_t seed, unsigned threads,
+                             uint8_t** ptrh, size_t* len, ph_build_stats* stats);
+void ph_free(void* p);
 
 /* Build statistics (stats.cpp:59-61; recorded by group_buckets, engine.hpp:304-322) on the
  * index's device, synchronous: hist[s] = number of the P*B buckets holding s of the u64 keys

@@ -80,13 +80,17 @@ def build_cpp_test(log):
     return out
 
 
+PRODUCT_SOURCES = ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_build.cu", "ph_sort.cu",
+                   "ph_builder.cu", "ph_abi.cu"]
+
+
 def build_variants(defs, log=None, force=False):
     """Tuning builds of the product with different compile-time knobs (tools/tune.py)."""
     os.makedirs(os.path.join(PKG, "variants"), exist_ok=True)
     outs = []
     for name, flags in defs.items():
         out = build_lib(os.path.join("variants", f"libph_gpu_{name}.so"),
-                        ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_build.cu", "ph_abi.cu"], extra=flags, log=log,
+                        PRODUCT_SOURCES, extra=flags, log=log,
                         force=force)
         outs.append(out)
     return outs
@@ -97,7 +101,7 @@ def main(force=False):
     os.makedirs(os.path.dirname(log), exist_ok=True)
     open(log, "w").close()
     libs = [
-        build_lib("libph_gpu.so", ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_build.cu", "ph_abi.cu"], log=log,
+        build_lib("libph_gpu.so", PRODUCT_SOURCES, log=log,
                   force=force),
         build_lib("libph_bench.so", ["ph_bench.cu"], log=log, force=force),
     ]

@@ -27,6 +27,7 @@
 #include "../../include/ph_gpu.h"
 #include "ph_device.cuh"
 #include "ph_kernels.h"
+#include "ph_nvtx.h"
 
 using u128 = unsigned __int128;
 
@@ -105,6 +106,12 @@ constexpr int kL2NoWindow = 2;        // no persisting access-policy window
 constexpr int kDefaultL2Flags = 0;
 
 }  // namespace
+
+namespace phg {
+// for ph_builder.cu: the thread-local error of this ABI, and the optimal-gamma table
+int report_error(int code, const std::string& msg) { return fail(code, msg); }
+void optimal_gamma_table(std::vector<uint64_t>& t) { optimal_table(t); }
+}  // namespace phg
 
 namespace {
 struct Pipeline;
@@ -545,6 +552,7 @@ int ph_gpu_set_launch(int threads, int bps) {
 }
 
 int ph_gpu_index_create(const uint8_t* ptrh, size_t len, int device, ph_gpu_index** out) {
+    PH_RANGE("ph_gpu_index_create");
     if (!out) return fail(PH_E_INVALID, "null out handle");
     *out = nullptr;
     Parsed p;
@@ -710,6 +718,7 @@ int ph_gpu_index_set_scratch_limit(ph_gpu_index* index, uint64_t bytes) {
 }
 
 int ph_gpu_index_set_l2_policy(ph_gpu_index* index, uint64_t hot_bytes, int flags) {
+    PH_RANGE("ph_gpu_index_set_l2_policy");
     if (!index) return fail(PH_E_INVALID, "null index");
     DeviceGuard g(index->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
@@ -734,6 +743,7 @@ int ph_gpu_index_info(const ph_gpu_index* index, ph_gpu_info* out) {
 
 int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, void* d_out,
                      int out_width, int minimal, ph_gpu_stream_t stream) {
+    PH_RANGE("ph_gpu_query_u64");
     if (!ix) return fail(PH_E_INVALID, "null index");
     if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
     if (int rc = check_width(out_width)) return rc;
@@ -760,6 +770,7 @@ int ph_gpu_query_u64(const ph_gpu_index* ix, const uint64_t* d_keys, size_t n, v
 int ph_gpu_query_bytes(const ph_gpu_index* ix, const uint8_t* d_bytes, const uint64_t* d_offsets,
                        size_t n, void* d_out, int out_width, int minimal,
                        ph_gpu_stream_t stream) {
+    PH_RANGE("ph_gpu_query_bytes");
     if (!ix) return fail(PH_E_INVALID, "null index");
     if (ix->info.key_kind != 1) return fail(PH_E_KEYKIND, "string query on a u64-key index");
     if (int rc = check_width(out_width)) return rc;
@@ -903,6 +914,7 @@ size_t chunk_keys(size_t n) {
 
 int ph_gpu_index_stream_u64(const ph_gpu_index* ix, const uint64_t* h_keys, size_t n, void* h_out,
                             int out_width, int minimal) {
+    PH_RANGE("ph_gpu_index_stream_u64");
     if (!ix) return fail(PH_E_INVALID, "null index");
     if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
     if (int rc = check_width(out_width)) return rc;
@@ -972,6 +984,7 @@ int ph_gpu_index_stream_u64(const ph_gpu_index* ix, const uint64_t* h_keys, size
 int ph_gpu_index_stream_bytes(const ph_gpu_index* ix, const uint8_t* h_bytes,
                               const uint64_t* h_offsets, size_t n, void* h_out, int out_width,
                               int minimal) {
+    PH_RANGE("ph_gpu_index_stream_bytes");
     if (!ix) return fail(PH_E_INVALID, "null index");
     if (ix->info.key_kind != 1) return fail(PH_E_KEYKIND, "string query on a u64-key index");
     if (int rc = check_width(out_width)) return rc;
@@ -1055,6 +1068,7 @@ int ph_gpu_index_stream_bytes(const ph_gpu_index* ix, const uint8_t* h_bytes,
 
 int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n_bases, int k,
                        void* d_out, int out_width, int minimal, ph_gpu_stream_t stream) {
+    PH_RANGE("ph_gpu_query_kmers");
     if (!ix) return fail(PH_E_INVALID, "null index");
     if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "k-mer query on a string-key index");
     if (k < 1 || k > 32) return fail(PH_E_INVALID, "k must be in [1, 32]");
@@ -1083,6 +1097,7 @@ int ph_gpu_query_kmers(const ph_gpu_index* ix, const uint64_t* d_seq, uint64_t n
 
 int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uint64_t n_bases,
                               int k, void* h_out, int out_width, int minimal) {
+    PH_RANGE("ph_gpu_index_stream_kmers");
     if (!ix) return fail(PH_E_INVALID, "null index");
     if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "k-mer query on a string-key index");
     if (k < 1 || k > 32) return fail(PH_E_INVALID, "k must be in [1, 32]");
@@ -1163,6 +1178,7 @@ int ph_gpu_index_stream_kmers(const ph_gpu_index* ix, const uint64_t* h_seq, uin
 // pinned block) and writes the answer into that block, and the call waits on the index's
 // single-key stream. Many host threads may call at once; they take turns on the block.
 int ph_gpu_index_u64(const ph_gpu_index* ix, uint64_t key, int minimal, uint64_t* out) {
+    PH_RANGE("ph_gpu_index_u64");
     if (!ix || !out) return fail(PH_E_INVALID, "null argument");
     if (ix->info.key_kind != 0) return fail(PH_E_KEYKIND, "u64 query on a string-key index");
     DeviceGuard g(ix->device);
@@ -1181,6 +1197,7 @@ int ph_gpu_index_u64(const ph_gpu_index* ix, uint64_t key, int minimal, uint64_t
 
 int ph_gpu_index_bytes(const ph_gpu_index* ix, const uint8_t* key, size_t len, int minimal,
                        uint64_t* out) {
+    PH_RANGE("ph_gpu_index_bytes");
     if (!ix || !out || (!key && len)) return fail(PH_E_INVALID, "null argument");
     if (ix->info.key_kind != 1) return fail(PH_E_KEYKIND, "string query on a u64-key index");
     DeviceGuard g(ix->device);
@@ -1214,6 +1231,7 @@ int ph_gpu_index_bytes(const ph_gpu_index* ix, const uint8_t* key, size_t len, i
 // (cudaHostRegister, read-only) so the upload runs at PCIe speed, then validated and
 // uploaded exactly as ph_gpu_index_create does.
 int ph_gpu_index_load(const char* path, int device, ph_gpu_index** out) {
+    PH_RANGE("ph_gpu_index_load");
     if (!path || !out) return fail(PH_E_INVALID, "null argument");
     *out = nullptr;
     const int fd = open(path, O_RDONLY);
@@ -1240,6 +1258,7 @@ int ph_gpu_index_load(const char* path, int device, ph_gpu_index** out) {
 // outputs >= n and repeated outputs among d_out[0..count).
 int ph_gpu_verify_bijection(const void* d_out, size_t count, int out_width, uint64_t n,
                             int device, uint64_t* out_of_range, uint64_t* duplicates) {
+    PH_RANGE("ph_gpu_verify_bijection");
     if (!d_out || !out_of_range || !duplicates) return fail(PH_E_INVALID, "null argument");
     if (int rc = check_width(out_width)) return rc;
     DeviceGuard g(device);
@@ -1266,6 +1285,7 @@ int ph_gpu_verify_bijection(const void* d_out, size_t count, int out_width, uint
 int ph_gpu_build_prepare_u64(const uint64_t* d_keys, size_t n, uint64_t parts,
                              uint64_t slots_per_part, uint64_t seed, int device,
                              uint64_t* d_hashes, uint64_t* d_offsets, int* status) {
+    PH_RANGE("ph_gpu_build_prepare_u64");
     if ((!d_keys && n) || (!d_hashes && n) || !d_offsets || !status)
         return fail(PH_E_INVALID, "null argument");
     if (parts == 0 || slots_per_part == 0) return fail(PH_E_INVALID, "degenerate shape");
@@ -1280,6 +1300,7 @@ int ph_gpu_build_prepare_u64(const uint64_t* d_keys, size_t n, uint64_t parts,
 
 int ph_gpu_bucket_sizes(const ph_gpu_index* index, const uint64_t* d_keys, size_t n,
                         uint64_t* hist, size_t cap, size_t* len) {
+    PH_RANGE("ph_gpu_bucket_sizes");
     if (!index || (!d_keys && n) || !len || (!hist && cap)) return fail(PH_E_INVALID, "null argument");
     if (index->info.key_kind != 0) return fail(PH_E_KEYKIND, "index was built over byte-string keys");
     DeviceGuard g(index->device);
@@ -1295,6 +1316,7 @@ int ph_gpu_bucket_sizes(const ph_gpu_index* index, const uint64_t* d_keys, size_
 
 int ph_gpu_gather_replay_u64(const ph_gpu_index* index, const uint64_t* d_keys, size_t n,
                              ph_gpu_stream_t stream) {
+    PH_RANGE("ph_gpu_gather_replay_u64");
     if (!index || (!d_keys && n)) return fail(PH_E_INVALID, "null argument");
     if (index->info.key_kind != 0) return fail(PH_E_KEYKIND, "index was built over byte-string keys");
     DeviceGuard g(index->device);

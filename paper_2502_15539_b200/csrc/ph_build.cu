@@ -10,12 +10,10 @@
 //                                               kDuplicateHashes on equal neighbours
 // part = hi(P * h) is monotone in h, so sorting all hashes by h gives exactly the
 // part-major arrangement with every part sorted. This file produces that array and the
-// part offsets on the device: a hash kernel, a device radix sort of the u64 hashes
-// (CUB, from the CUDA toolkit: construction is off the hot path), and a kernel that writes
-// the part boundaries and checks both failure conditions.
+// part offsets on the device: the hand-written MSD radix sort of ph_sort.cu (which hashes
+// the keys in its first pass), and a kernel that writes the part boundaries and checks both
+// failure conditions.
 #include <cuda_runtime.h>
-
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cstdint>
@@ -83,33 +81,23 @@ static cudaError_t scratch_pool(cudaMemPool_t* pool) {
     return cudaSuccess;
 }
 
+cudaError_t sort_hashes_u64(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out,
+                            uint64_t* tmp, cudaMemPool_t pool, cudaStream_t s);
+
 cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint64_t S,
                               uint64_t seed, uint64_t* hashes, uint64_t* offsets, int* status,
                               cudaStream_t s, int sms) {
     *status = 0;
     int* d_status = nullptr;
     uint64_t* tmp = nullptr;
-    void* cub_tmp = nullptr;
-    size_t cub_bytes = 0;
     cudaMemPool_t pool = nullptr;
     cudaError_t e = scratch_pool(&pool);
     if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&d_status, sizeof(int), pool, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_status, 0, sizeof(int), s);
     if (e == cudaSuccess && n) e = cudaMallocFromPoolAsync(&tmp, n * 8, pool, s);
     const int grid = sms * 8;
-    if (e == cudaSuccess && n) {
-        k_hash_u64<<<grid, 256, 0, s>>>(keys, n, seed, tmp);
-        note_launch();
-        e = cudaGetLastError();
-    }
-    // sort tmp -> hashes (all 64 bits: the part is the high-order function of h)
-    if (e == cudaSuccess && n)
-        e = cub::DeviceRadixSort::SortKeys(nullptr, cub_bytes, tmp, hashes, n, 0, 64, s);
-    if (e == cudaSuccess && n) e = cudaMallocFromPoolAsync(&cub_tmp, cub_bytes, pool, s);
-    if (e == cudaSuccess && n) {
-        e = cub::DeviceRadixSort::SortKeys(cub_tmp, cub_bytes, tmp, hashes, n, 0, 64, s);
-        note_launch();
-    }
+    // hashes = sorted C*(key^seed) (all 64 bits: the part is the high-order function of h)
+    if (e == cudaSuccess && n) e = sort_hashes_u64(keys, n, seed, hashes, tmp, pool, s);
     if (e == cudaSuccess) {
         k_part_bounds<<<grid, 256, 0, s>>>(hashes, n, P, offsets, d_status);
         note_launch();
@@ -122,7 +110,6 @@ cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint
     }
     int h_status = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if (cub_tmp) cudaFreeAsync(cub_tmp, s);
     if (tmp) cudaFreeAsync(tmp, s);
     if (d_status) cudaFreeAsync(d_status, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);

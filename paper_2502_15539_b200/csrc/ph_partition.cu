@@ -35,6 +35,7 @@
 
 #include "ph_device.cuh"
 #include "ph_kernels.h"
+#include "ph_nvtx.h"
 
 namespace phg {
 
@@ -859,6 +860,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
     cudaFuncSetAttribute(k_bin<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
     const uint64_t want = L.ntiles;
     const int grid_a = (int)(want < (uint64_t)sms * kBinCtas ? want : (uint64_t)sms * kBinCtas);
+    nvtx_mark("partitioned: pass A (bin)");
     const bool tma = G <= (uint32_t)kTmaGroups && !std::getenv("PH_GPU_NO_TMA") &&
                      (src_kind == 1 || (reinterpret_cast<uintptr_t>(keys) & 15) == 0);
     if (tma) {
@@ -890,6 +892,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
     // B: the query arithmetic (and remap_slot) over the group regions, one L2-resident
     // pilot slice after another
     pt_record(1, s);
+    nvtx_mark("partitioned: pass B (query regions)");
     const int b_per_sm = env_int("PH_GPU_PART_B_CTAS", 4);
     e = out_width == 4
             ? launch_regions(ix, gamma_kind, pow2, G, L.cap, L.nent, ctrl, bins,
@@ -899,6 +902,7 @@ cudaError_t launch_query_partitioned(const DevIndex& ix0, int gamma_kind, bool p
     if (e != cudaSuccess) return e;
     pt_record(2, s);
     // C: back to input order
+    nvtx_mark("partitioned: pass C (unbin)");
     const size_t sm4 = UnbinTma<uint32_t>::kSmem, sm8 = UnbinTma<uint64_t>::kSmem;
     cudaFuncSetAttribute(k_unbin_tma<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
     cudaFuncSetAttribute(k_unbin_tma<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm8);

@@ -80,7 +80,7 @@ except AttributeError:
     pass
 
 # status codes (ph_gpu.h)
-OK, E_INVALID, E_FORMAT, E_CUDA, E_KEYKIND, E_NOMEM, E_UNSUPPORTED = range(7)
+OK, E_INVALID, E_FORMAT, E_CUDA, E_KEYKIND, E_NOMEM, E_UNSUPPORTED, E_DUPLICATE, E_BUILD_FAILED = range(9)
 
 
 class PhGpuError(RuntimeError):
@@ -145,6 +145,124 @@ def build_prepare_u64(keys, parts: int, slots_per_part: int, seed: int, device: 
                                        C.c_void_p(hashes.data_ptr() if n else 0),
                                        C.c_void_p(offsets.data_ptr()), C.byref(st)))
     return hashes, offsets, st.value
+
+
+# ---- construction: ph_gpu_build_u64 --------------------------------------
+
+BUCKET_FN = {"linear": 0, "quadratic": 1, "cubic": 2, "skewed": 3, "optimal": 4}
+REMAP = {"plain32": 0, "cacheline-ef": 1, "clef": 1, "elias-fano": 2, "ef": 2}
+REDUCE = {"pow2-mul": 0, "fastmod-single": 1, "fastmod-multi": 2}
+
+
+class BuildParams(C.Structure):
+    """BuildParams (shape.hpp:46-56); parts/slots_per_part/buckets_per_part force a shape."""
+    _fields_ = [
+        ("alpha_num", C.c_uint32), ("alpha_den", C.c_uint32),
+        ("lambda_num", C.c_uint32), ("lambda_den", C.c_uint32),
+        ("bucket_fn", C.c_uint8), ("remap_kind", C.c_uint8), ("reduce_kind", C.c_uint8),
+        ("reserved", C.c_uint8), ("max_seed_retries", C.c_uint32), ("seed", C.c_uint64),
+        ("parts", C.c_uint64), ("slots_per_part", C.c_uint64), ("buckets_per_part", C.c_uint64),
+    ]
+
+
+class BuildStats(C.Structure):
+    """BuildStats (build.hpp:10-45) plus per-stage wall times."""
+    _fields_ = [
+        ("n", C.c_uint64), ("parts", C.c_uint64), ("slots_per_part", C.c_uint64),
+        ("buckets_per_part", C.c_uint64), ("seed", C.c_uint64), ("attempts", C.c_uint32),
+        ("remap_kind", C.c_uint8), ("remap_fell_back", C.c_uint8), ("reserved", C.c_uint8 * 2),
+        ("total_evictions", C.c_uint64), ("evictions_by_percentile", C.c_uint64 * 100),
+        ("pilot_bytes", C.c_uint64), ("remap_payload_bytes", C.c_uint64),
+        ("upload_ms", C.c_double), ("prepare_ms", C.c_double), ("search_ms", C.c_double),
+        ("remap_ms", C.c_double), ("total_ms", C.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("reserved", "evictions_by_percentile")}
+        d["evictions_by_percentile"] = list(self.evictions_by_percentile)
+        return d
+
+
+_L.ph_build_preset.argtypes = [C.c_char_p, C.POINTER(BuildParams)]
+_L.ph_build_compute_shape.argtypes = [C.c_uint64, C.POINTER(BuildParams), u64p, u64p, u64p]
+_L.ph_gpu_build_u64.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(BuildParams), C.c_uint, C.c_int,
+                                C.POINTER(u8p), C.POINTER(C.c_size_t), C.POINTER(BuildStats)]
+_L.ph_build_from_sorted_u64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(BuildParams),
+                                        C.c_uint64, C.c_uint, C.POINTER(u8p),
+                                        C.POINTER(C.c_size_t), C.POINTER(BuildStats)]
+_L.ph_free.argtypes = [C.c_void_p]
+
+
+def build_params(preset="default", *, lambda_=None, alpha=None, bucket_fn=None, remap=None,
+                 reduce=None, seed=None, retries=None, shape=None) -> BuildParams:
+    """preset() (shape.cpp:65-84) with the same overrides as the reference's BuildParams."""
+    p = BuildParams()
+    _check(_L.ph_build_preset(preset.encode(), C.byref(p)))
+    if lambda_ is not None:
+        p.lambda_num, p.lambda_den = lambda_
+    if alpha is not None:
+        p.alpha_num, p.alpha_den = alpha
+    if bucket_fn is not None:
+        p.bucket_fn = BUCKET_FN[bucket_fn] if isinstance(bucket_fn, str) else bucket_fn
+    if remap is not None:
+        p.remap_kind = REMAP[remap] if isinstance(remap, str) else remap
+    if reduce is not None:
+        p.reduce_kind = REDUCE[reduce] if isinstance(reduce, str) else reduce
+    if seed is not None:
+        p.seed = seed
+    if retries is not None:
+        p.max_seed_retries = retries
+    if shape is not None:
+        p.parts, p.slots_per_part, p.buckets_per_part = shape
+    return p
+
+
+def compute_shape(n: int, params: BuildParams):
+    P, S, B = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    _check(_L.ph_build_compute_shape(n, C.byref(params), C.byref(P), C.byref(S), C.byref(B)))
+    return P.value, S.value, B.value
+
+
+def _take_ptrh(ptr, ln) -> bytes:
+    try:
+        return C.string_at(ptr, ln.value)
+    finally:
+        _L.ph_free(ptr)
+
+
+def build_u64(keys, params: BuildParams | None = None, threads: int = 0, device: int = 0,
+              stats: bool = False):
+    """build(keys, params, threads) + serialize() (construction.cpp:139-143): PTRH v1 bytes.
+    `keys` is a numpy u64 array (host) or a CUDA int64/uint64 tensor (device)."""
+    params = params if params is not None else build_params()
+    if _is_torch(keys):
+        if _dtype_name(keys) not in ("int64", "uint64") or not _contiguous(keys):
+            raise ValueError("keys must be a contiguous int64/uint64 tensor")
+        ptr, n = (keys.data_ptr() if keys.numel() else None), keys.numel()
+    else:
+        keys = np.ascontiguousarray(keys)
+        if keys.dtype not in (np.uint64, np.int64):
+            raise ValueError("keys must be a uint64/int64 array")
+        ptr, n = (keys.ctypes.data if keys.size else None), keys.size
+    out, ln, st = u8p(), C.c_size_t(0), BuildStats()
+    _check(_L.ph_gpu_build_u64(C.c_void_p(ptr), n, C.byref(params), threads, device, C.byref(out),
+                               C.byref(ln), C.byref(st)))
+    b = _take_ptrh(out, ln)
+    return (b, st.as_dict()) if stats else b
+
+
+def build_from_sorted_u64(hashes: np.ndarray, offsets: np.ndarray, params: BuildParams, seed: int,
+                          threads: int = 0, stats: bool = False):
+    """The host stage of one build attempt (no GPU): sorted part-major hashes + part offsets
+    -> PTRH bytes, or PhGpuError(E_BUILD_FAILED) if a part cannot be placed."""
+    hashes = np.ascontiguousarray(hashes, dtype=np.uint64)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    out, ln, st = u8p(), C.c_size_t(0), BuildStats()
+    _check(_L.ph_build_from_sorted_u64(C.c_void_p(hashes.ctypes.data), C.c_void_p(offsets.ctypes.data),
+                                       hashes.size, C.byref(params), seed, threads, C.byref(out),
+                                       C.byref(ln), C.byref(st)))
+    b = _take_ptrh(out, ln)
+    return (b, st.as_dict()) if stats else b
 
 
 def set_pass_timing(on: bool):

@@ -1,0 +1,239 @@
+"""Construction: ph_gpu_build_u64 / ph_build_from_sorted_u64 produce the same
+PTRH bytes as the reference's build() + serialize() (construction.cpp:139-152,
+serde.cpp:142-170) for the same keys and parameters.
+
+CPU: the host stage (per-part pilot search, remap assembly, serialization; engine.hpp:105-557)
+fed with the numpy restatement of the front phases, against the reference's own build, for
+every bucket function, remap kind and reduce kind, forced shapes and the error paths
+(mirrors test_construction.cpp and test_shape.cpp). GPU: the whole build, with the front on
+the device (hand-written sort, ph_sort.cu), host- and device-resident keys, reseeding,
+duplicate keys, and skewed hash sets that exercise every split level of the sort."""
+import numpy as np
+import pytest
+
+from oracle.bindings import build_prepare_u64_np, corpus_u64_np
+
+CASES = [
+    ("default", dict(lambda_=(30, 10))),
+    ("default", {}),
+    ("fast", {}),
+    ("compact", {}),
+    ("default", dict(bucket_fn="linear", lambda_=(30, 10))),
+    ("default", dict(bucket_fn="quadratic")),
+    ("default", dict(bucket_fn="skewed", remap="elias-fano")),
+    ("default", dict(bucket_fn="optimal", remap="plain32")),
+    ("compact", dict(reduce="pow2-mul")),
+    ("fast", dict(reduce="pow2-mul", remap="elias-fano")),
+    ("default", dict(reduce="fastmod-single")),
+    ("default", dict(alpha=(98, 100), lambda_=(42, 10))),
+]
+
+
+def _ph():
+    from paper_2502_15539_b200 import ph_gpu
+    return ph_gpu
+
+
+def _seed_of(ptrh: bytes) -> int:
+    return int.from_bytes(ptrh[48:56], "little")
+
+
+def _host_build(ph, keys, gp, threads=0):
+    """The attempt loop of build_u64_impl (construction.cpp:113-138) with the numpy front."""
+    P, S, _ = (gp.parts, gp.slots_per_part, gp.buckets_per_part) if gp.parts else \
+        ph.compute_shape(keys.size, gp)
+    seed = gp.seed
+    for attempt in range(gp.max_seed_retries + 1):
+        h, off, st = build_prepare_u64_np(keys, P, S, seed)
+        if st == 2:
+            raise ph.PhGpuError(ph.E_DUPLICATE, "duplicate keys")
+        if st == 0:
+            try:
+                return ph.build_from_sorted_u64(h, off, gp, seed, threads=threads)
+            except ph.PhGpuError as e:
+                if e.code != ph.E_BUILD_FAILED:
+                    raise
+        seed = (0x517CC1B727220A95 * ((seed ^ attempt) ^ 0x9E3779B97F4A7C15)) & ((1 << 64) - 1)
+    raise ph.PhGpuError(ph.E_BUILD_FAILED, "all attempts failed")
+
+
+@pytest.mark.parametrize("preset,kw", CASES)
+def test_host_stage_matches_reference(ref, preset, kw):
+    ph = _ph()
+    keys = corpus_u64_np(0, 150_000, 91)
+    want = ref.build_u64(keys, ref.params(preset, **kw))
+    gp = ph.build_params(preset, **kw)
+    assert ph.compute_shape(keys.size, gp) == ref.shape(keys.size, ref.params(preset, **kw))
+    got = _host_build(ph, keys, gp, threads=4)
+    assert got == want, (preset, kw)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 45, 1000, 44 * 37])
+def test_host_stage_tiny(ref, n):
+    ph = _ph()
+    keys = corpus_u64_np(0, n, 92)
+    for preset in ("default", "fast"):
+        assert _host_build(ph, keys, ph.build_params(preset)) == ref.build_u64(keys, ref.params(preset)), (n, preset)
+
+
+@pytest.mark.parametrize("shape", [(1, 6000, 1700), (7, 800, 250), (16, 1 << 9, 180), (3, 1877, 2000)])
+def test_host_stage_forced_shape(ref, shape):
+    """build_with_shape (construction.cpp:145-152), including tight shapes that need reseeds."""
+    ph = _ph()
+    keys = corpus_u64_np(0, 5000, 93)
+    P, S, B = shape
+    want = ref.build_u64_shape(keys, ref.params("default", lambda_=(30, 10)), P, S, B)
+    got = _host_build(ph, keys, ph.build_params("default", lambda_=(30, 10), shape=shape))
+    assert got == want, shape
+
+
+def test_reseed_path_matches_reference(ref):
+    """A shape tight enough that the first seeds fail (oversubscribed parts or failed
+    placement): the accepted seed and the bytes equal the reference's."""
+    ph = _ph()
+    keys = corpus_u64_np(0, 4000, 94)
+    shape = (8, 520, 170)  # 4160 slots for 4000 keys: the default seed fails
+    rp = ref.params("fast", retries=30)
+    want = ref.build_u64_shape(keys, rp, *shape)
+    got = _host_build(ph, keys, ph.build_params("fast", retries=30, shape=shape))
+    assert got == want
+    assert _seed_of(want) != rp.seed  # the case really reseeded
+
+
+def test_hopeless_shape_fails_like_reference(ref):
+    ph = _ph()
+    keys = corpus_u64_np(0, 4000, 94)
+    with pytest.raises(RuntimeError):
+        ref.build_u64_shape(keys, ref.params("fast", retries=2, alpha=(1, 1)), 1, 4000, 1)
+    with pytest.raises(ph.PhGpuError) as e:
+        _host_build(ph, keys, ph.build_params("fast", retries=2, shape=(1, 4000, 1), alpha=(1, 1)))
+    assert e.value.code == ph.E_BUILD_FAILED
+
+
+def test_compute_shape_matches_reference(ref):
+    ph = _ph()
+    for n in [1, 2, 100, 79_999, 80_000, 80_001, 10**6, 10**7, 10**8, 10**9, 3 * 10**8, 2**32 - 1]:
+        for preset, kw in CASES:
+            try:
+                want = ref.shape(n, ref.params(preset, **kw))
+            except ValueError:
+                with pytest.raises(ph.PhGpuError):
+                    ph.compute_shape(n, ph.build_params(preset, **kw))
+                continue
+            assert ph.compute_shape(n, ph.build_params(preset, **kw)) == want, (n, preset, kw)
+
+
+def test_invalid_params_rejected():
+    ph = _ph()
+    keys = corpus_u64_np(0, 100, 95)
+    h, off, _ = build_prepare_u64_np(keys, 1, 200, 1)
+    bad = [dict(alpha=(0, 100)), dict(alpha=(101, 100)), dict(lambda_=(9, 10)),
+           dict(alpha=(995, 1000))]  # CacheLineEF needs alpha <= 0.99 (shape.cpp:58-62)
+    for kw in bad:
+        with pytest.raises(ph.PhGpuError) as e:
+            ph.build_from_sorted_u64(h, off, ph.build_params("default", **kw), 1)
+        assert e.value.code == ph.E_INVALID, kw
+    with pytest.raises(ph.PhGpuError) as e:
+        ph.build_params("nope")
+    assert e.value.code == ph.E_INVALID
+    with pytest.raises(ph.PhGpuError) as e:  # fewer slots than keys
+        ph.build_from_sorted_u64(h, off, ph.build_params("default", shape=(1, 50, 20)), 1)
+    assert e.value.code == ph.E_INVALID
+
+
+# ---- GPU: the whole build ----
+
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset,kw", CASES)
+def test_gpu_build_matches_reference(ref, preset, kw):
+    torch = _cuda()
+    ph = _ph()
+    keys = corpus_u64_np(0, 300_000, 96)
+    want = ref.build_u64(keys, ref.params(preset, **kw))
+    before = ph.launch_count()
+    got, st = ph.build_u64(keys, ph.build_params(preset, **kw), stats=True)
+    assert ph.launch_count() > before  # the front ran on the device
+    assert got == want, (preset, kw)
+    assert st["n"] == keys.size and st["attempts"] >= 1
+    # device-resident keys give the same bytes
+    d = torch.from_numpy(keys.view(np.int64)).cuda()
+    assert ph.build_u64(d, ph.build_params(preset, **kw)) == want
+
+
+@pytest.mark.gpu
+def test_gpu_build_reseed_and_errors(ref):
+    _cuda()
+    ph = _ph()
+    keys = corpus_u64_np(0, 4000, 94)
+    shape = (8, 520, 170)
+    want = ref.build_u64_shape(keys, ref.params("fast", retries=30), *shape)
+    assert ph.build_u64(keys, ph.build_params("fast", retries=30, shape=shape)) == want
+    dup = corpus_u64_np(0, 50_000, 97)
+    dup[-1] = dup[17]
+    with pytest.raises(ph.PhGpuError) as e:
+        ph.build_u64(dup)
+    assert e.value.code == ph.E_DUPLICATE
+    with pytest.raises(ph.PhGpuError) as e:  # one bucket of 4000 keys: no pilot is collision-free
+        ph.build_u64(keys, ph.build_params("fast", retries=2, shape=(1, 4000, 1), alpha=(1, 1)))
+    assert e.value.code == ph.E_BUILD_FAILED
+    with pytest.raises(ph.PhGpuError) as e:
+        ph.build_u64(keys[:0])
+    assert e.value.code == ph.E_INVALID
+
+
+@pytest.mark.gpu
+def test_gpu_build_large_matches_reference(ref):
+    """n = 2e7: 16 parts of ~1.2 M keys, two split levels in the device sort, the pinned
+    transfer ring in several chunks; byte-identical to the reference's build."""
+    _cuda()
+    ph = _ph()
+    keys = corpus_u64_np(0, 20_000_000, 42)
+    rp = ref.params("default", lambda_=(30, 10))
+    want = ref.build_u64(keys, rp)
+    got, st = ph.build_u64(keys, ph.build_params("default", lambda_=(30, 10)), stats=True)
+    assert got == want
+    assert st["prepare_ms"] > 0 and st["search_ms"] > 0
+
+
+def _keys_for_hashes(ref, h: np.ndarray, seed: int) -> np.ndarray:
+    """Keys whose hashes C*(key^seed) are exactly h (C is odd, so invertible mod 2^64)."""
+    cinv = np.uint64(ref.L.ref_mix_constant_inverse())
+    with np.errstate(over="ignore"):
+        return (h.astype(np.uint64) * cinv) ^ np.uint64(seed)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["narrow", "clustered", "repeated", "uniform_big"])
+def test_gpu_sort_skewed_hash_sets(ref, kind):
+    """The device MSD sort on hash sets that defeat its fast path: all hashes in a 2^20
+    window (every split level and the redo path down to the last 12 bits), clusters of
+    equal high bits with bins over 64 keys, many repeated values (duplicates), and a
+    uniform set large enough for two split levels. Compared with numpy's sort."""
+    torch = _cuda()
+    ph = _ph()
+    rng = np.random.default_rng(7)
+    seed = 0x9E3779B97F4A7C15
+    if kind == "narrow":
+        h = np.uint64(0xABCDE) << np.uint64(40) | rng.integers(0, 1 << 20, 300_000, dtype=np.uint64)
+    elif kind == "clustered":
+        hi = rng.integers(0, 64, 400_000, dtype=np.uint64) << np.uint64(50)
+        h = hi | (rng.integers(0, 1 << 10, 400_000, dtype=np.uint64) << np.uint64(20)) | \
+            rng.integers(0, 1 << 20, 400_000, dtype=np.uint64)
+    elif kind == "repeated":
+        h = rng.integers(0, 1000, 200_000, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    else:
+        h = rng.integers(0, 2**63, 30_000_000, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    keys = _keys_for_hashes(ref, h, seed)
+    P, S = 5, 10**9
+    want_h, want_off, want_st = build_prepare_u64_np(keys, P, S, seed)
+    got_h, got_off, st = ph.build_prepare_u64(torch.from_numpy(keys.view(np.int64)).cuda(), P, S, seed)
+    assert st == want_st
+    assert np.array_equal(got_h.cpu().numpy().view(np.uint64), want_h), kind
+    assert np.array_equal(got_off.cpu().numpy().view(np.uint64), want_off), kind

@@ -35,6 +35,10 @@ def main():
     ap.add_argument("--no-persist", action="store_true",
                     help="drop the persisting-L2 carve-out after the index is created")
     a = ap.parse_args()
+    for k, v in dict(construction=False, verify="none", cpu_sample=0, no_cpu_baseline=True, no_replay=True,
+                     secondary_configs=False, steps=1, warmup=0, impl="ours").items():
+        if not hasattr(a, k):  # attributes bench.py's workloads read from its own parser
+            setattr(a, k, v)
     cfg = dict(bench.CONFIGS[a.config])
     if a.n:
         cfg["n"] = a.n

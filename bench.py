@@ -163,8 +163,10 @@ class ClockSampler:
         for s in loaded:
             bits |= s[2]
         reasons = sorted(name for b, name in REASONS.items() if bits & b and name != "gpu_idle")
+        capped = sum(1 for s in loaded if s[2] & 0x4)  # sw_power_cap bit
         return {"sm_mhz": statistics.median(s[1] for s in loaded), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(loaded)}
+                "sm_min_mhz": min(s[1] for s in loaded), "reasons": reasons, "samples": len(loaded),
+                "sw_power_cap_share": round(capped / len(loaded), 3)}
 
 
 # ---------------------------------------------------------------------------

@@ -138,6 +138,59 @@ __global__ void __launch_bounds__(256) k_gather_skew(const uint8_t* __restrict__
     if (acc == 0x7fffffffu) *sink = acc;
 }
 
+// L1->XBAR port model (pass B's bound): per gather (uniform random 1-byte
+// load over [0, F), evict_last), IN coalesced 8-byte words streamed in (evict_first) and one
+// OUT-byte coalesced store (.cs; OUT = 0, 4 or 8). Measures how the L2-resident gather rate
+// falls as streamed sectors share the SM's request port with the gathers.
+template <int IN, int OUT>
+__global__ void __launch_bounds__(256, 4) k_port(const uint8_t* __restrict__ buf, uint64_t F,
+                                                 uint64_t nloads, uint64_t seed,
+                                                 const uint64_t* __restrict__ sin, void* sout,
+                                                 uint32_t* sink) {
+    uint64_t pk, pc;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pk));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pc));
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t acc = 0;
+    for (uint64_t base = warp * 256; base + 256 <= nloads; base += nwarps * 256) {
+        uint64_t kv[8];
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            kv[j] = 0;
+#pragma unroll
+            for (int w = 0; w < IN; w++) {
+                uint64_t t;
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+                             : "=l"(t) : "l"(sin + (base + j * 32 + lane) * IN + w), "l"(pc));
+                kv[j] ^= t;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t r = mix64(seed + (base + j * 32 + lane) * kGolden + (IN ? (kv[j] & 1) : 0));
+            uint16_t x;
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+                         : "=h"(x) : "l"(buf + __umul64hi(r, F)), "l"(pk));
+            v[j] = x;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            if (OUT == 4)
+                asm volatile("st.global.cs.u32 [%0], %1;" ::"l"((uint32_t*)sout + base + j * 32 + lane),
+                             "r"(v[j] + (uint32_t)kv[j]) : "memory");
+            else if (OUT == 8)
+                asm volatile("st.global.cs.u64 [%0], %1;" ::"l"((uint64_t*)sout + base + j * 32 + lane),
+                             "l"(kv[j] + v[j]) : "memory");
+            else
+                acc += v[j] + (uint32_t)kv[j];
+        }
+    }
+    if (acc == 0x7fffffffu) *sink = acc;
+}
+
 // Uniform random gather with a selectable load flavour (DRAM fetch-size experiments).
 template <int MODE>
 __device__ __forceinline__ uint16_t ld_mode(const uint8_t* p, uint64_t pol) {
@@ -415,6 +468,24 @@ int phb_gather_skew(const uint8_t* d_buf, uint64_t F_hot, uint64_t F, double p_h
     k_gather_skew<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(d_buf, F_hot, F, ph, nloads, seed,
                                                             mode, d_sink, d_sin, d_sout);
     return (int)cudaGetLastError();
+}
+
+// in_words in {0,1,2}, out_bytes in {0,4,8}; d_sin holds nloads*in_words words, d_sout
+// nloads*out_bytes bytes. Launches 4 CTAs of 256 threads per SM (pass B's shape).
+int phb_port_model(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t seed, int in_words,
+                   int out_bytes, const uint64_t* d_sin, void* d_sout, uint32_t* d_sink,
+                   void* stream) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const cudaStream_t s = (cudaStream_t)stream;
+#define PH_PORT(I, O)                                                                        \
+    if (in_words == I && out_bytes == O) {                                                   \
+        k_port<I, O><<<sms * 4, 256, 0, s>>>(d_buf, F, nloads, seed, d_sin, d_sout, d_sink); \
+        return (int)cudaGetLastError();                                                      \
+    }
+    PH_PORT(0, 0) PH_PORT(1, 0) PH_PORT(2, 0) PH_PORT(0, 4) PH_PORT(1, 4) PH_PORT(1, 8) PH_PORT(2, 4) PH_PORT(2, 8)
+#undef PH_PORT
+    return (int)cudaErrorInvalidValue;
 }
 
 // Context-wide L2 knobs for the tuning sweeps (tools/tune.py).

@@ -26,8 +26,12 @@ def main():
     ap.add_argument("--out", default=os.path.join(os.path.dirname(os.path.dirname(
         os.path.abspath(__file__))), "profiles", "r02_traffic.json"))
     a = ap.parse_args()
-    raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if a.report.endswith(".csv"):  # `ncu -i X.ncu-rep --page raw --csv` already run on the GPU box
+        with open(a.report) as f:
+            raw = f.read()
+    else:
+        raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     col = {m: hdr.index(m) for m in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",

@@ -14,6 +14,7 @@ import json
 import os
 import subprocess
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -69,6 +70,9 @@ def child(a):
         ts = []
         ph_gpu.set_pass_timing(True)
         for _ in range(a.reps):
+            if a.gap_ms:  # idle gap between steps (power / clock headroom probe)
+                torch.cuda.synchronize()
+                time.sleep(a.gap_ms / 1e3)
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -96,6 +100,7 @@ def main():
     ap.add_argument("--strings", action="store_true", help="config-4 strings on an aes64 index")
     ap.add_argument("--nq", type=int, default=0, help="queries (default: the shape's n)")
     ap.add_argument("--ncu", action="store_true", help="child only: one call per mode")
+    ap.add_argument("--gap-ms", type=float, default=0.0, help="idle time between timed steps")
     ap.add_argument("--child", action="store_true")
     a = ap.parse_args()
     if a.child:
@@ -112,7 +117,7 @@ def main():
                 k, v = item.split("=", 1)
                 env[k] = v
             cmd = [sys.executable, __file__, "--child", "--config", str(a.config), "--runs", "-",
-                   "--reps", str(a.reps), "--nq", str(a.nq)] + (["--kmers"] if a.kmers else []) + \
+                   "--reps", str(a.reps), "--nq", str(a.nq), "--gap-ms", str(a.gap_ms)] + (["--kmers"] if a.kmers else []) + \
                 (["--strings"] if a.strings else [])
             p = subprocess.run(cmd, env=env, capture_output=True, text=True)
             line = [x for x in p.stdout.splitlines() if x.startswith("RESULT ")]

@@ -108,8 +108,22 @@ __global__ void __launch_bounds__(256) k_remap_patch(const DevIndex ix, const Re
         const uint32_t c = min(rl.counts[w], lcap);
         const uint64_t* li = rl.idx + (uint64_t)w * lcap;
         const uint64_t* lr = rl.rem + (uint64_t)w * lcap;
-        for (uint32_t e = lane; e < c; e += 32)
-            out[li[e]] = (OutT)remap_get(ix, lr[e]);  // remap_slot, index.hpp:98-100
+        // four entries per lane in flight: the list reads, the decodes' table reads and the
+        // patch stores of a round are independent (a list holds ~200 entries at config 2)
+        for (uint32_t e0 = 0; e0 < c; e0 += 128) {
+            uint64_t i4[4], r4[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t e = e0 + q * 32 + lane;
+                i4[q] = e < c ? li[e] : 0;
+                r4[q] = e < c ? lr[e] : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t e = e0 + q * 32 + lane;
+                if (e < c) out[i4[q]] = (OutT)remap_get(ix, r4[q]);  // remap_slot, index.hpp:98-100
+            }
+        }
     }
 }
 

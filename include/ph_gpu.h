@@ -189,6 +189,12 @@ int ph_build_compute_shape(uint64_t n, const ph_build_params* params, uint64_t* 
 int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* params,
                      unsigned threads, int device, uint8_t** ptrh, size_t* len,
                      ph_build_stats* stats);
+/* Where ph_gpu_build_u64 runs the per-part pilot search (engine.hpp:105-292): 0 (default) on
+ * the GPU, one CTA per part (csrc/ph_search.cu), falling back to host threads for shapes the
+ * kernel does not take (slots_per_part beyond the shared-memory bitmap, a bucket over 64
+ * keys); 1 always on host threads; 2 on the GPU or PH_E_UNSUPPORTED. Either way the bytes are
+ * the reference's; ph_build_stats.reserved[0] = 1 reports a GPU search. */
+int ph_gpu_set_build_search(int mode);
 /* The host stage of one attempt under `seed` (no GPU): hashes[0..n) are the attempt's sorted
  * hashes in part-major order and offsets[parts+1] the part boundaries (what
  * ph_gpu_build_prepare_u64 returns). PH_E_BUILD_FAILED if a part cannot be placed. */

@@ -81,7 +81,7 @@ def build_cpp_test(log):
 
 
 PRODUCT_SOURCES = ["ph_query.cu", "ph_query_bytes.cu", "ph_partition.cu", "ph_build.cu", "ph_sort.cu",
-                   "ph_builder.cu", "ph_abi.cu"]
+                   "ph_builder.cu", "ph_search.cu", "ph_abi.cu"]
 
 
 def build_variants(defs, log=None, force=False):

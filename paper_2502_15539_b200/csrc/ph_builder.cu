@@ -693,6 +693,49 @@ Arith make_arith(const Shape& sh, const ph_build_params& p, const std::vector<ui
     return a;
 }
 
+// Where the pilot search of ph_gpu_build_u64 runs: 0 = on the GPU when the shape allows it
+// (ph_search.cu), else on host threads; 1 = always host threads; 2 = GPU or PH_E_UNSUPPORTED.
+std::atomic<int> g_search_mode{0};
+
+// The free / overflow slot lists of every part from the GPU search's occupancy bitmaps
+// (engine.hpp:324-343), parts in parallel.
+void results_from_bitmaps(const Shape& sh, const std::vector<uint32_t>& taken, uint32_t words,
+                          unsigned threads, std::vector<PartResult>& parts) {
+    parts.assign(sh.P, PartResult{});
+    std::atomic<uint64_t> next{0};
+    const unsigned T = (unsigned)std::min<uint64_t>(thread_count(threads), std::max<uint64_t>(1, sh.P));
+    std::vector<std::thread> ws;
+    for (unsigned t = 0; t < T; t++)
+        ws.emplace_back([&] {
+            for (;;) {
+                const uint64_t p = next.fetch_add(1);
+                if (p >= sh.P) break;
+                const uint32_t* tk = taken.data() + p * words;
+                const uint64_t base = p * sh.S;
+                PartResult& out = parts[p];
+                for (uint64_t s0 = 0; s0 < sh.S; s0 += 32) {
+                    const uint32_t wv = tk[s0 >> 5];
+                    const uint32_t lim = (uint32_t)std::min<uint64_t>(32, sh.S - s0);
+                    if (base + s0 + lim <= sh.n) {  // all below n: the free ones
+                        uint32_t fr = ~wv & (lim == 32 ? 0xffffffffu : (1u << lim) - 1);
+                        while (fr) {
+                            out.free_slots.push_back(base + s0 + (uint32_t)__builtin_ctz(fr));
+                            fr &= fr - 1;
+                        }
+                    } else {
+                        for (uint32_t b = 0; b < lim; b++) {
+                            const bool t1 = (wv >> b) & 1;
+                            const uint64_t g = base + s0 + b;
+                            if (t1 && g >= sh.n) out.overflow_slots.push_back(g);
+                            else if (!t1 && g < sh.n) out.free_slots.push_back(g);
+                        }
+                    }
+                }
+            }
+        });
+    for (auto& t : ws) t.join();
+}
+
 Shape resolve_shape(uint64_t n, const ph_build_params& p) {
     if (!p.parts && !p.slots_per_part && !p.buckets_per_part) return make_shape(n, p);
     // build_with_shape (construction.cpp:145-152)
@@ -864,7 +907,74 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                  "build_prepare_u64");
             prep_ms += ms_since(tp);
             if (status == 2) throw BuildFail(PH_E_DUPLICATE, "duplicate keys in input");
-            if (status == 0) {
+            bool searched = false;
+            if (status == 0 && g_search_mode.load() != 1) {
+                // the pilot search on the GPU (ph_search.cu): one CTA per part
+                std::vector<uint64_t> hoff(sh.P + 1);
+                cuda(cudaMemcpy(hoff.data(), d_off, (sh.P + 1) * 8, cudaMemcpyDeviceToHost), "part offsets");
+                uint64_t maxpart = 0;
+                for (uint64_t p = 0; p < sh.P; p++) maxpart = std::max(maxpart, hoff[p + 1] - hoff[p]);
+                const bool can = phg::search_parts_supported(sh.S, sh.B, maxpart);
+                if (!can && g_search_mode.load() == 2)
+                    throw BuildFail(PH_E_UNSUPPORTED, "the GPU pilot search does not take this shape");
+                if (can) {
+                    tp = std::chrono::steady_clock::now();
+                    const uint32_t words = (uint32_t)((sh.S + 31) / 32);
+                    uint8_t* d_pilots = nullptr;
+                    uint32_t* d_taken = nullptr;
+                    uint64_t* d_opt = nullptr;
+                    struct Free {
+                        uint8_t*& a;
+                        uint32_t*& b;
+                        uint64_t*& c;
+                        ~Free() {
+                            if (a) cudaFree(a);
+                            if (b) cudaFree(b);
+                            if (c) cudaFree(c);
+                        }
+                    } fr{d_pilots, d_taken, d_opt};
+                    cuda(cudaMalloc(&d_pilots, sh.P * sh.B), "device pilots");
+                    cuda(cudaMalloc(&d_taken, sh.P * (uint64_t)words * 4), "device occupancy bitmaps");
+                    if (!opt.empty()) {
+                        cuda(cudaMalloc(&d_opt, opt.size() * 8), "device gamma table");
+                        cuda(cudaMemcpy(d_opt, opt.data(), opt.size() * 8, cudaMemcpyHostToDevice), "gamma table");
+                    }
+                    unsigned long long hst[4] = {}, hpct[100] = {};
+                    cuda(phg::search_parts_gpu(d_h, d_off, n, sh.P, sh.S, sh.B, seed, params->bucket_fn, d_opt,
+                                               maxpart, d_pilots, d_taken, hst, hpct, nullptr, sms),
+                         "search_parts_gpu");
+                    if (hst[1] && g_search_mode.load() == 2)
+                        throw BuildFail(PH_E_UNSUPPORTED, "the GPU pilot search gave up on this key set");
+                    if (!hst[1]) {
+                        searched = true;
+                        if (!hst[0]) {  // every part placed
+                            std::vector<uint8_t> pilots(sh.P * sh.B);
+                            std::vector<uint32_t> taken(sh.P * (uint64_t)words);
+                            cuda(cudaMemcpy(pilots.data(), d_pilots, pilots.size(), cudaMemcpyDeviceToHost), "pilots");
+                            cuda(cudaMemcpy(taken.data(), d_taken, taken.size() * 4, cudaMemcpyDeviceToHost),
+                                 "occupancy bitmaps");
+                            std::vector<PartResult> parts;
+                            results_from_bitmaps(sh, taken, words, threads, parts);
+                            search_ms += ms_since(tp);
+                            const std::vector<uint8_t> out = finish(sh, *params, seed, pilots, parts, stats);
+                            if (stats) {
+                                stats->n = n, stats->parts = sh.P, stats->slots_per_part = sh.S;
+                                stats->buckets_per_part = sh.B, stats->seed = seed, stats->attempts = attempt + 1;
+                                stats->total_evictions = hst[3];
+                                for (int i = 0; i < 100; i++) stats->evictions_by_percentile[i] = hpct[i];
+                                stats->upload_ms = upload_ms, stats->prepare_ms = prep_ms;
+                                stats->search_ms = search_ms, stats->total_ms = ms_since(t0);
+                                stats->reserved[0] = 1;  // the search ran on the GPU
+                            }
+                            if (!(*ptrh = to_malloc(out))) throw std::bad_alloc();
+                            *len = out.size();
+                            return PH_OK;
+                        }
+                        search_ms += ms_since(tp);  // a part failed: reseed
+                    }
+                }
+            }
+            if (status == 0 && !searched) {
                 tp = std::chrono::steady_clock::now();
                 DeviceFeed feed;
                 cuda(feed.start(d_h, d_off, sh.P), "hash transfer ring");
@@ -900,6 +1010,12 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
     if (d_h) cudaFree(d_h);
     if (d_off) cudaFree(d_off);
     return rc;
+}
+
+int ph_gpu_set_build_search(int mode) {
+    if (mode < 0 || mode > 2) return phg::report_error(PH_E_INVALID, "mode must be 0, 1 or 2");
+    g_search_mode.store(mode);
+    return PH_OK;
 }
 
 void ph_free(void* p) { std::free(p); }

@@ -96,6 +96,15 @@ cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint
                               uint64_t seed, uint64_t* hashes, uint64_t* offsets, int* status,
                               cudaStream_t s, int sms);
 
+// ph_search.cu: the per-part pilot search on the GPU (one CTA per part, 256 pilots at once).
+size_t search_smem_bytes(uint64_t S);
+bool search_parts_supported(uint64_t S, uint64_t B, uint64_t max_part);
+cudaError_t search_parts_gpu(const uint64_t* d_hashes, const uint64_t* d_off, uint64_t n, uint64_t P,
+                             uint64_t S, uint64_t B, uint64_t seed, int fn, const uint64_t* d_opt,
+                             uint64_t max_part, uint8_t* d_pilots, uint32_t* d_taken,
+                             unsigned long long* h_status, unsigned long long* h_by_pct,
+                             cudaStream_t s, int sms);
+
 // Bucket-size histogram of a key set (stats.cpp:59-61): hist_out[s] for s < min(cap, *len).
 cudaError_t bucket_size_hist(const DevIndex& ix, int gamma_kind, const uint64_t* keys, uint64_t n,
                              uint64_t* hist_out, uint64_t cap, uint64_t* len_out, cudaStream_t s,

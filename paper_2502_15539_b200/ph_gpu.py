@@ -180,6 +180,7 @@ class BuildStats(C.Structure):
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("reserved", "evictions_by_percentile")}
         d["evictions_by_percentile"] = list(self.evictions_by_percentile)
+        d["search_on_gpu"] = bool(self.reserved[0])
         return d
 
 
@@ -191,6 +192,13 @@ _L.ph_build_from_sorted_u64.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.PO
                                         C.c_uint64, C.c_uint, C.POINTER(u8p),
                                         C.POINTER(C.c_size_t), C.POINTER(BuildStats)]
 _L.ph_free.argtypes = [C.c_void_p]
+_L.ph_gpu_set_build_search.argtypes = [C.c_int]
+
+
+def set_build_search(mode: int):
+    """Where build_u64 runs the pilot search: 0 GPU with host fallback (default), 1 host
+    threads, 2 GPU or PhGpuError(E_UNSUPPORTED)."""
+    _check(_L.ph_gpu_set_build_search(mode))
 
 
 def build_params(preset="default", *, lambda_=None, alpha=None, bucket_fn=None, remap=None,

@@ -150,9 +150,18 @@ def _cuda():
     return torch
 
 
+@pytest.fixture(params=[1, 2], ids=["host_search", "gpu_search"])
+def search_mode(request):
+    """Both homes of the pilot search: host threads (1) and the GPU kernel (2, no fallback)."""
+    ph = _ph()
+    ph.set_build_search(request.param)
+    yield request.param
+    ph.set_build_search(0)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("preset,kw", CASES)
-def test_gpu_build_matches_reference(ref, preset, kw):
+def test_gpu_build_matches_reference(ref, preset, kw, search_mode):
     torch = _cuda()
     ph = _ph()
     keys = corpus_u64_np(0, 300_000, 96)
@@ -162,13 +171,35 @@ def test_gpu_build_matches_reference(ref, preset, kw):
     assert ph.launch_count() > before  # the front ran on the device
     assert got == want, (preset, kw)
     assert st["n"] == keys.size and st["attempts"] >= 1
+    assert st["search_on_gpu"] == (search_mode == 2)
     # device-resident keys give the same bytes
     d = torch.from_numpy(keys.view(np.int64)).cuda()
     assert ph.build_u64(d, ph.build_params(preset, **kw)) == want
 
 
 @pytest.mark.gpu
-def test_gpu_build_reseed_and_errors(ref):
+def test_gpu_search_stats_match_host_search(ref):
+    """Evictions (total and by percentile of first placements) are a trace of the search's
+    order and choices: the GPU search reports the host search's numbers exactly."""
+    _cuda()
+    ph = _ph()
+    keys = corpus_u64_np(0, 2_000_000, 91)
+    bp = ph.build_params("compact")  # lambda 4.0: evictions in every part
+    try:
+        ph.set_build_search(1)
+        b1, s1 = ph.build_u64(keys, bp, stats=True)
+        ph.set_build_search(2)
+        b2, s2 = ph.build_u64(keys, bp, stats=True)
+    finally:
+        ph.set_build_search(0)
+    assert b1 == b2 == ref.build_u64(keys, ref.params("compact"))
+    assert s2["search_on_gpu"] and not s1["search_on_gpu"]
+    assert s1["total_evictions"] == s2["total_evictions"] > 0
+    assert s1["evictions_by_percentile"] == s2["evictions_by_percentile"]
+
+
+@pytest.mark.gpu
+def test_gpu_build_reseed_and_errors(ref, search_mode):
     _cuda()
     ph = _ph()
     keys = corpus_u64_np(0, 4000, 94)
@@ -182,14 +213,14 @@ def test_gpu_build_reseed_and_errors(ref):
     assert e.value.code == ph.E_DUPLICATE
     with pytest.raises(ph.PhGpuError) as e:  # one bucket of 4000 keys: no pilot is collision-free
         ph.build_u64(keys, ph.build_params("fast", retries=2, shape=(1, 4000, 1), alpha=(1, 1)))
-    assert e.value.code == ph.E_BUILD_FAILED
+    assert e.value.code == ph.E_BUILD_FAILED  # in either home of the search
     with pytest.raises(ph.PhGpuError) as e:
         ph.build_u64(keys[:0])
     assert e.value.code == ph.E_INVALID
 
 
 @pytest.mark.gpu
-def test_gpu_build_large_matches_reference(ref):
+def test_gpu_build_large_matches_reference(ref, search_mode):
     """n = 2e7: 16 parts of ~1.2 M keys, two split levels in the device sort, the pinned
     transfer ring in several chunks; byte-identical to the reference's build."""
     _cuda()

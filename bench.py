@@ -305,11 +305,12 @@ class U64Work:
             self.construction = {
                 "what": "build(keys) + serialize() of this config's index from host-resident keys: "
                         "the reference's build() on all host threads vs ph_gpu_build_u64 "
-                        "(hash + MSD radix sort + part offsets on the GPU, pilot search on all "
-                        "host threads); wall clock, one run each",
+                        "(hash + MSD radix sort + part offsets and the per-part pilot search on "
+                        "the GPU, remap table on the host); wall clock, one run each",
                 "n": int(keys.size), "reference_s": round(ref_s, 3), "ours_s": round(ours_s, 3),
                 "speedup": round(ref_s / ours_s, 3), "host_threads": int(ref_threads),
                 "identical_ptrh": same, "attempts": st["attempts"],
+                "search_on_gpu": bool(st.get("search_on_gpu")),
                 "stages_ms": {k: round(st[k], 1) for k in
                               ("upload_ms", "prepare_ms", "search_ms", "remap_ms", "total_ms")}}
 

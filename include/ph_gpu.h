@@ -168,7 +168,7 @@ typedef struct ph_build_stats {
     uint64_t pilot_bytes, remap_payload_bytes;
     double upload_ms;   /* host keys -> device */
     double prepare_ms;  /* GPU: hash + sort + part offsets, all attempts */
-    double search_ms;   /* pilot search over all parts (overlapping the hash transfer) */
+    double search_ms;   /* pilot search over all parts (GPU kernel + copy back, or host threads) */
     double remap_ms;    /* remap table + serialization */
     double total_ms;
 } ph_build_stats;
@@ -181,9 +181,9 @@ int ph_build_compute_shape(uint64_t n, const ph_build_params* params, uint64_t* 
 /* build(span<const uint64_t>, params, threads, stats) + serialize() (construction.cpp:139-143,
  * serde.cpp:142-170): the PTRH v1 bytes of the index over the distinct keys keys[0..n), which
  * may be host or device memory. Each attempt hashes and sorts on `device`
- * (ph_gpu_build_prepare_u64) and runs the per-part pilot search on `threads` host threads
- * (0 = all), fed part by part from the device. The bytes equal the reference's for the same
- * keys and parameters. *ptrh is malloc'ed: release it with ph_free. Errors: PH_E_INVALID
+ * (ph_gpu_build_prepare_u64) and runs the per-part pilot search there too (one CTA per part,
+ * csrc/ph_search.cu; ph_gpu_set_build_search), or on `threads` host threads (0 = all) fed part
+ * by part from the device. The bytes equal the reference's for the same keys and parameters. *ptrh is malloc'ed: release it with ph_free. Errors: PH_E_INVALID
  * (bad parameters or shape, empty key set), PH_E_DUPLICATE, PH_E_BUILD_FAILED, PH_E_CUDA,
  * PH_E_NOMEM. */
 int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* params,

@@ -26,6 +26,8 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <queue>
@@ -940,9 +942,12 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                         cuda(cudaMemcpy(d_opt, opt.data(), opt.size() * 8, cudaMemcpyHostToDevice), "gamma table");
                     }
                     unsigned long long hst[4] = {}, hpct[100] = {};
+                    const bool trace = std::getenv("PH_GPU_BUILD_TRACE") != nullptr;
+                    const double t_alloc = ms_since(tp);
                     cuda(phg::search_parts_gpu(d_h, d_off, n, sh.P, sh.S, sh.B, seed, params->bucket_fn, d_opt,
                                                maxpart, d_pilots, d_taken, hst, hpct, nullptr, sms),
                          "search_parts_gpu");
+                    const double t_kernel = ms_since(tp);
                     if (hst[1] && g_search_mode.load() == 2)
                         throw BuildFail(PH_E_UNSUPPORTED, "the GPU pilot search gave up on this key set");
                     if (!hst[1]) {
@@ -953,8 +958,13 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                             cuda(cudaMemcpy(pilots.data(), d_pilots, pilots.size(), cudaMemcpyDeviceToHost), "pilots");
                             cuda(cudaMemcpy(taken.data(), d_taken, taken.size() * 4, cudaMemcpyDeviceToHost),
                                  "occupancy bitmaps");
+                            const double t_copy = ms_since(tp);
                             std::vector<PartResult> parts;
                             results_from_bitmaps(sh, taken, words, threads, parts);
+                            if (trace)
+                                std::fprintf(stderr, "[ph_gpu build] search: alloc %.1f ms, kernel+workspace %.1f ms, "
+                                             "copy back %.1f ms, slot lists %.1f ms\n", t_alloc, t_kernel - t_alloc,
+                                             t_copy - t_kernel, ms_since(tp) - t_copy);
                             search_ms += ms_since(tp);
                             const std::vector<uint8_t> out = finish(sh, *params, seed, pilots, parts, stats);
                             if (stats) {

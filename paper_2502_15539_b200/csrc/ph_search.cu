@@ -31,6 +31,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "ph_device.cuh"
@@ -50,6 +52,7 @@ struct Arith {
     uint64_t P, S, B, seed, fm;  // fm = floor((2^64 - 1) / S)
     const uint64_t* opt;
     int fn, p2;
+    ModFast mf;                  // 32-bit form of y mod S for 2^13 <= S < 2^21 (ph_arith.cuh)
 };
 
 __device__ __forceinline__ uint64_t gamma_rt(const Arith& a, uint64_t x) {
@@ -68,6 +71,7 @@ __device__ __forceinline__ uint32_t bucket_in_part(const Arith& a, uint64_t h) {
 // slot within the part: reduce(y), the exact y mod S, or the pow2 form (reduce.hpp:67-72)
 __device__ __forceinline__ uint32_t slot_of_y(const Arith& a, uint64_t y) {
     if (a.p2) return (uint32_t)(__umul64hi(kC, y) & (a.S - 1));
+    if (a.mf.ok) return mod_fast(y, a.mf.S, a.mf.nS, a.mf.c, a.mf.m1, a.mf.m2);
     uint64_t r = y - __umul64hi(y, a.fm) * a.S;
     while (r >= a.S) r -= a.S;
     return (uint32_t)r;
@@ -91,6 +95,11 @@ struct Shared {
     unsigned long long wkey[kSThreads / 32];
     unsigned long long costs[256];         // a big bucket's eviction cost per pilot
     uint32_t bad[8];                       // ... and the pilots ruled out
+    uint32_t bsl[kSThreads / 32][kMaxK];   // batch mode: each warp's winning pilot's slots
+    uint32_t bwin[kSThreads / 32];         //             its pilot (32 = none of the first 32)
+    uint32_t bkc[kSThreads / 32];          //             its bucket's size
+    uint32_t bsel[kSThreads / 32];         //             the warp that won each bucket
+    uint32_t ncommit;
     uint32_t esl[kMaxK];                   // the evicting pilot's slots
     uint32_t recent[kRecent];
     unsigned long long heap[kHeapCap];
@@ -136,8 +145,60 @@ __device__ __forceinline__ bool distinct(const uint32_t* s, uint32_t k) {
     return true;
 }
 
+// free_pilot's test of one pilot for a bucket of at most KB keys, the slots in registers
+// (a per-thread array indexed at run time lives in local memory, and with ~210 KB of the SM's
+// 256 KB carved out for the two CTAs' bitmaps the L1 cannot hold it: every read went to L2).
+constexpr int kRegK = 8;
+template <int KB>
+__device__ __forceinline__ bool test_pilot_reg(const Arith& a, const uint32_t* taken,
+                                               const uint64_t* kq, uint32_t kc, uint64_t hl,
+                                               uint32_t (&r)[KB]) {
+    uint32_t busy = 0;  // no early exit: the kc slot computations are independent chains
+#pragma unroll
+    for (int i = 0; i < KB; i++) {
+        r[i] = 0xffffffffu - i;  // beyond kc: distinct dummies (slots are < 2^31)
+        if (i < (int)kc) {
+            r[i] = slot_of_y(a, kq[i] ^ hl);
+            busy |= taken[r[i] >> 5] >> (r[i] & 31);
+        }
+    }
+    bool ok = !(busy & 1);
+    if (ok) {
+#pragma unroll
+        for (int i = 1; i < KB; i++)
+#pragma unroll
+            for (int j = 0; j < i; j++) ok &= r[i] != r[j];
+    }
+    return ok;
+}
+
+// Smallest lane of `cand` (lanes whose pilot's slots sl[0..k) are all free) whose slots are
+// pairwise distinct, or 32: the candidate writes its slots to the warp's shared row and lane i
+// compares slot i with the slots before it (O(k) per candidate instead of a k^2 loop over a
+// local-memory array). Leaves the winner's slots in row[0..k). k <= 32.
+__device__ __forceinline__ uint32_t first_distinct(unsigned cand, const uint32_t* sl, uint32_t k,
+                                                   uint32_t* row, unsigned lane) {
+    while (cand) {
+        const uint32_t l0 = (uint32_t)__ffs(cand) - 1;
+        if (lane == l0)
+            for (uint32_t i = 0; i < k; i++) row[i] = sl[i];
+        __syncwarp();
+        bool dup = false;
+        if (lane < k) {
+            const uint32_t mine = row[lane];
+            for (uint32_t j = 0; j < lane; j++) dup |= row[j] == mine;
+        }
+        const bool anyd = __any_sync(kFull, dup);
+        __syncwarp();
+        if (!anyd) return l0;
+        cand &= cand - 1;
+    }
+    return 32;
+}
+
 // status[0]: a part failed (reseed); status[1]: unsupported shape (host search);
 // status[2]: next part to claim; status[3]: total evictions; by_pct: 100 counters.
+__device__ unsigned long long g_prof[16];  // cycles: prologue, batch steps, full steps; counts
 __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
     const Arith a, const uint64_t* __restrict__ hashes, const uint64_t* __restrict__ off,
     uint8_t* __restrict__ pilots, uint32_t* __restrict__ taken_out, uint32_t words,
@@ -173,6 +234,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
         uint8_t* pl = pilots + (uint64_t)part * B;
 
         // ---- prologue ------------------------------------------------------------------
+        long long t_p0 = clock64(), t_batch = 0, t_full = 0, n_batch = 0, n_full = 0;
         for (uint32_t i = tid; i < words; i += kSThreads) taken[i] = 0;
         for (uint32_t i = tid; i < S; i += kSThreads) {
             w.owner[i] = kNoBucket;
@@ -256,16 +318,169 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
         __syncthreads();
 
         // ---- main loop -----------------------------------------------------------------
+        const long long t_pro = clock64() - t_p0;
         uint32_t cursor = 0, kcur = kMaxK, rpos = 0, part_ev = 0, tag_base = 0;
         while (kcur > 1 && sm.cnt[kcur] == 0) kcur--;
 
         const uint64_t budget = 10ull * S;
-        bool failed = false;
+        bool failed = false, single = false;
+        uint32_t wpb = 1;  // batch mode: warps (x 32 pilots) per bucket
+        uint32_t cend = 0;  // end of the current size class in the visiting order
         for (;;) {
             // next bucket: the larger of the heap's top and the visiting order's head
             const uint32_t hn = sm.hn;
             if (cursor == nonempty && hn == 0) break;
-            while (cursor >= nbig && cursor < nonempty && cursor >= sm.cbeg[kcur] + sm.cnt[kcur]) kcur--;
+            if (cursor >= nbig && cursor < nonempty && cursor >= cend) {
+                while (cursor >= sm.cbeg[kcur] + sm.cnt[kcur]) kcur--;
+                cend = sm.cbeg[kcur] + sm.cnt[kcur];  // (kept in a register between steps)
+            }
+            if (!single && hn == 0 && cursor >= nbig && cursor < nonempty) {
+                // Batch mode (no evicted bucket pending): the next 8 / wpb buckets at once,
+                // wpb warps (32 * wpb pilots) per bucket, each against the bitmap as it
+                // stands. They commit in visiting order; a bucket commits if its pilot's
+                // slots are still free after the earlier commits of the batch (bits are only
+                // set here, so no smaller pilot can have become free: the choice is the
+                // sequential search's). A bucket that lost a slot restarts the next batch; one
+                // that found no pilot doubles wpb, and at 256 pilots goes to the full step
+                // below (an eviction). Batches whose winners sit in the lower half of their
+                // pilot range halve wpb.
+                const long long t_b0 = clock64();
+                const uint32_t nb = min(8u / wpb, nonempty - cursor);
+                const uint32_t q = warp / wpb, c = cursor + q;
+                uint32_t kc = kcur, mybk = 0;
+                if (q < nb) {
+                    if (c >= cend)
+                        while (c >= sm.cbeg[kc] + sm.cnt[kc]) kc--;
+                    mybk = w.ord[c];
+                    const uint64_t* kq = w.hre + sm.cpos[kc] + (uint64_t)(c - sm.cbeg[kc]) * kc;
+                    const uint32_t pil = (warp % wpb) * 32 + lane;
+                    const uint64_t hl = kC * ((uint64_t)pil ^ a.seed);
+                    bool ok = true;
+                    uint32_t r8[kRegK];
+                    if (kc <= 2) {  // (warp-uniform: the bucket is the warp's)
+                        uint32_t r2[2];
+                        ok = test_pilot_reg<2>(a, taken, kq, kc, hl, r2);
+                        r8[0] = r2[0], r8[1] = r2[1];
+                    } else if (kc <= 4) {
+                        uint32_t r4[4];
+                        ok = test_pilot_reg<4>(a, taken, kq, kc, hl, r4);
+#pragma unroll
+                        for (int i = 0; i < 4; i++) r8[i] = r4[i];
+                    } else if (kc <= kRegK) {
+                        ok = test_pilot_reg<kRegK>(a, taken, kq, kc, hl, r8);
+                    } else {
+                        for (uint32_t i = 0; i < kc; i++) {
+                            const uint32_t s1 = slot_of_y(a, kq[i] ^ hl);
+                            if ((taken[s1 >> 5] >> (s1 & 31)) & 1) {
+                                ok = false;
+                                break;
+                            }
+                            sl[i] = s1;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(kFull, ok);
+                    uint32_t win;
+                    if (kc <= kRegK) {
+                        win = bal ? (uint32_t)__ffs(bal) - 1 : 32u;
+                        if (lane == win) {
+#pragma unroll
+                            for (int i = 0; i < kRegK; i++)
+                                if (i < (int)kc) sm.bsl[warp][i] = r8[i];
+                        }
+                    } else {
+                        win = first_distinct(bal, sl, kc, sm.bsl[warp], lane);
+                    }
+                    if (lane == 0) {
+                        sm.bwin[warp] = win < 32 ? (warp % wpb) * 32 + win : 256u;
+                        sm.bkc[warp] = kc;
+                    }
+                    if (tid == 0) {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(kq + 192));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(w.ord + cursor + 256));
+                    }
+                }
+                __syncthreads();
+                // Commit. Common case: every bucket up to the first one without a pilot
+                // claims its slots at once (one atomicOr per slot); a claim that finds its bit
+                // set lost the slot to another bucket of the batch, and then all claims are
+                // rolled back and warp 0 commits the batch serially in visiting order.
+                // lane x < 8 holds warp x's result; a segmented minimum over each bucket's wpb
+                // warps gives every bucket's pilot and the warp holding it (pilot << 8 | warp)
+                uint32_t pv = lane < 8 && lane / wpb < nb ? sm.bwin[lane] << 8 | lane : 256u << 8 | (lane & 7);
+                for (uint32_t o = 1; o < wpb; o <<= 1) pv = min(pv, __shfl_xor_sync(kFull, pv, o));
+                const unsigned lead = lane < 8 && lane % wpb == 0 && lane / wpb < nb;  // one lane per bucket
+                const unsigned none = __ballot_sync(kFull, lead && (pv >> 8) == 256);
+                const uint32_t nf = none ? ((uint32_t)__ffs(none) - 1) / wpb : nb;
+                const unsigned high = __ballot_sync(kFull, lead && lane / wpb < nf && (pv >> 8) >= 16 * wpb);
+                const uint32_t mybw = __shfl_sync(kFull, pv, (q * wpb) & 7) & 0xff;
+                if (warp == 0 && lead && lane / wpb < nf) sm.bsel[lane / wpb] = pv & 0xff;
+                bool hit = false, claimed = false;
+                uint32_t s2 = 0;
+                if (q < nf && warp == mybw && lane < kc) {
+                    s2 = sm.bsl[warp][lane];
+                    hit = (atomicOr(&taken[s2 >> 5], 1u << (s2 & 31)) >> (s2 & 31)) & 1;
+                    claimed = !hit;
+                }
+                if (tid == 0) {
+                    sm.ncommit = nf | (nf < nb ? 1u : 0u) << 8 | (!high ? 1u << 16 : 0);
+                    if (((cursor + nf) & 4095) < nf && *(volatile unsigned long long*)status) sm.flags |= 1;
+                }
+                const int anyhit = __syncthreads_or(hit);
+                if (anyhit) {
+                    if (claimed) atomicAnd(&taken[s2 >> 5], ~(1u << (s2 & 31)));
+                    __syncthreads();
+                if (warp == 0) {
+                    uint32_t nc = 0, maxwin = 0, why = 0;  // why: 1 = no pilot, 2 = lost a slot
+                    for (; nc < nb; nc++) {
+                        uint32_t bw = nc * wpb;  // the bucket's warp holding the smallest pilot
+                        for (uint32_t x = 1; x < wpb; x++)
+                            if (sm.bwin[nc * wpb + x] < sm.bwin[bw]) bw = nc * wpb + x;
+                        const uint32_t pw = sm.bwin[bw], kq = sm.bkc[bw];
+                        if (pw == 256) {
+                            why = 1;
+                            break;
+                        }
+                        const uint32_t s1 = lane < kq ? sm.bsl[bw][lane] : 0;
+                        const bool hit = lane < kq && ((taken[s1 >> 5] >> (s1 & 31)) & 1);
+                        if (__any_sync(kFull, hit)) {
+                            why = 2;
+                            break;
+                        }
+                        if (lane < kq) atomicOr(&taken[s1 >> 5], 1u << (s1 & 31));
+                        __syncwarp();
+                        maxwin = max(maxwin, pw);
+                        if (lane == 0) sm.bsel[nc] = bw;
+                    }
+                    if (lane == 0) {
+                        sm.ncommit = nc | why << 8 | (maxwin < 16 * wpb ? 1u << 16 : 0);
+                        if (((cursor + nc) & 4095) < nc && *(volatile unsigned long long*)status) sm.flags |= 1;
+                    }
+                }
+                __syncthreads();
+                }
+                const uint32_t nc = sm.ncommit & 0xff, why = (sm.ncommit >> 8) & 0xff;
+                if (q < nc && sm.bsel[q] == warp) {  // the winning warp publishes
+                    if (lane < kc) w.owner[sm.bsl[warp][lane]] = mybk;
+                    if (lane == 0) pl[mybk] = (uint8_t)sm.bwin[warp];
+                }
+                cursor += nc;
+                if (why == 1) {
+                    if (wpb == 8) single = true;
+                    else wpb *= 2;
+                } else if (why == 0 && (sm.ncommit >> 16) && wpb > 1) {
+                    wpb /= 2;
+                }
+                if (sm.flags) {
+                    failed = true;
+                    break;
+                }
+                t_batch += clock64() - t_b0;
+                n_batch++;
+                continue;
+            }
+            single = false;
+            const long long t_f0 = clock64();
+            n_full++;
             uint32_t bk = 0, k = 0;
             const uint64_t* kh;
             bool from_heap = false;
@@ -405,16 +620,28 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
             }
             // free_pilot (engine.hpp:131-147): thread p tests pilot p
             bool ok = true;
-            for (uint32_t i = 0; i < k; i++) {
-                const uint32_t s = slot_of_y(a, kh[i] ^ hp);
-                if ((taken[s >> 5] >> (s & 31)) & 1) {
-                    ok = false;
-                    break;
+            if (k <= kRegK) {
+                uint32_t r8[kRegK];
+                ok = test_pilot_reg<kRegK>(a, taken, kh, k, hp, r8);
+                if (ok) {
+#pragma unroll
+                    for (int i = 0; i < kRegK; i++) sl[i] = r8[i];
                 }
-                sl[i] = s;
+            } else {
+                for (uint32_t i = 0; i < k; i++) {
+                    const uint32_t s = slot_of_y(a, kh[i] ^ hp);
+                    if ((taken[s >> 5] >> (s & 31)) & 1) {
+                        ok = false;
+                        break;
+                    }
+                    sl[i] = s;
+                }
             }
-            if (ok) ok = distinct(sl, k);
-            const unsigned bal = __ballot_sync(kFull, ok);
+            unsigned bal = __ballot_sync(kFull, ok);
+            if (k > kRegK) {
+                const uint32_t l0 = first_distinct(bal, sl, k, sm.bsl[warp], lane);
+                bal = l0 < 32 ? 1u << l0 : 0u;
+            }
             if (lane == 0) sm.wmin[warp] = bal ? warp * 32 + (__ffs(bal) - 1) : 256u;
             __syncthreads();  // B1 (every thread has read the heap's top)
             uint32_t pstar = 256;
@@ -499,6 +726,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                 }
                 rpos = (rpos + 1) % kRecent;
             }
+            t_full += clock64() - t_f0;
             if (!from_heap) cursor++;
             if (tid == 0 && (cursor & 1023) == 0 && !from_heap && *(volatile unsigned long long*)status)
                 sm.flags |= 1;  // another part failed: the attempt is over
@@ -519,6 +747,14 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
         // ---- epilogue: the part's occupancy bitmap and statistics ----------------------
         uint32_t* to = taken_out + (uint64_t)part * words;
         for (uint32_t i = tid; i < words; i += kSThreads) to[i] = taken[i];
+        if (tid == 0) {
+            atomicAdd(g_prof + 0, (unsigned long long)t_pro);
+            atomicAdd(g_prof + 1, (unsigned long long)t_batch);
+            atomicAdd(g_prof + 2, (unsigned long long)t_full);
+            atomicAdd(g_prof + 3, (unsigned long long)n_batch);
+            atomicAdd(g_prof + 4, (unsigned long long)n_full);
+            atomicAdd(g_prof + 5, 1ull);
+        }
         if (tid == 0 && sm.evictions) atomicAdd(status + 3, (unsigned long long)sm.evictions);
         if (tid < 100 && sm.by_pct[tid]) atomicAdd(by_pct + tid, (unsigned long long)sm.by_pct[tid]);
     }
@@ -550,6 +786,8 @@ cudaError_t search_parts_gpu(const uint64_t* d_hashes, const uint64_t* d_off, ui
     a.fm = a.p2 ? 0 : ~0ull / S;
     a.opt = d_opt;
     a.fn = fn;
+    a.mf = mod_fast_make(S);
+    if (a.p2) a.mf.ok = false;
     const uint32_t words = (uint32_t)((S + 31) / 32);
     const size_t smem = search_smem_bytes(S);
     cudaError_t e = cudaFuncSetAttribute(k_search_parts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -589,6 +827,15 @@ cudaError_t search_parts_gpu(const uint64_t* d_hashes, const uint64_t* d_off, ui
     }
     e = cudaMemcpyAsync(d_works, hw.data(), sizeof(Work) * grid, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_status, 0, (4 + 100) * 8, s);
+    const bool trace = std::getenv("PH_GPU_BUILD_TRACE") != nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (trace) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, s);
+    }
     if (e == cudaSuccess) {
         k_search_parts<<<grid, kSThreads, smem, s>>>(a, d_hashes, d_off, d_pilots, d_taken, words, d_works,
                                                      d_status, d_status + 4);
@@ -597,7 +844,20 @@ cudaError_t search_parts_gpu(const uint64_t* d_hashes, const uint64_t* d_off, ui
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_status, d_status, 4 * 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_by_pct, d_status + 4, 100 * 8, cudaMemcpyDeviceToHost, s);
+    if (trace) cudaEventRecord(ev1, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (trace && e == cudaSuccess) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        unsigned long long pr[16] = {};
+        cudaMemcpyFromSymbol(pr, g_prof, sizeof(pr));
+        const double parts = pr[5] ? (double)pr[5] : 1.0;
+        std::fprintf(stderr, "[ph_gpu search] kernel %.1f ms, grid %d; per part: prologue %.0f kcyc, batch steps "
+                     "%.0f (%.0f kcyc), full steps %.0f (%.0f kcyc)\n", ms, grid, pr[0] / parts / 1e3,
+                     pr[3] / parts, pr[1] / parts / 1e3, pr[4] / parts, pr[2] / parts / 1e3);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+    }
     cleanup();
     return e;
 }

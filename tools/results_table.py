@@ -1,6 +1,7 @@
 """Regenerates DESIGN.md §4's results table, the partition-pass summary, the config-3
-speed-ups and README.md's results rows from the committed bench lines
-(profiles/r01_bench_config*.json, profiles/r01_bench_reference_config3.json).
+speed-ups and README.md's results rows from the committed round-2 bench lines
+(profiles/r02_bench_config{1,2,3}.json — config 3's line carries configs 4 and 5 as
+`secondary` blocks — and profiles/r02_bench_reference_config3.json).
 
   python tools/results_table.py
 """
@@ -12,13 +13,21 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def load(name):
     with open(os.path.join(ROOT, "profiles", name)) as f:
-        return json.load(f)
+        return json.loads(f.read().strip().splitlines()[-1])
 
 
 def main():
-    d = {c: load(f"r01_bench_config{c}.json") for c in (1, 2, 3, 4, 5)}
-    r = load("r01_bench_reference_config3.json")
+    d = {c: load(f"r02_bench_config{c}.json") for c in (1, 2, 3)}
+    d[4] = d[3]["secondary"]["config4"]
+    d[5] = d[3]["secondary"]["config5"]
+    r = load("r02_bench_reference_config3.json")
     d3, d5 = d[3], d[5]
+
+    def bound(x):
+        k = x.get("dominant_kernel")
+        if not k:
+            return "— (L1 data pipe, §3)"
+        return f"{k['frac']:.2f} ({k['frac_vs_gather_only']:.2f})"
 
     def row(c, label, extra=""):
         x = d[c]
@@ -26,8 +35,7 @@ def main():
         v = f"**{x['value']:.1f}**" if c == 3 else f"{x['value']:.1f}"
         e = f"**{x['e2e']['value']:.2f}**" if c == 3 else f"{x['e2e']['value']:.2f}"
         return (f"| {label} | {v} ({ms} ms) | {x['nonminimal']['value']:.1f} | {e} | "
-                f"{x['cpu_baseline']['value']:.2f} | {x['roofline']['frac']:.2f}{extra} | "
-                f"{x['gather_roofline']['frac']:.2f} |")
+                f"{x['cpu_baseline']['value']:.2f} | {x['roofline']['frac']:.2f}{extra} | {bound(x)} |")
 
     table = "\n".join([
         row(3, "**3 (headline)** | 1e9 u64, shuffled; partitioned path (default layout)"),
@@ -37,12 +45,15 @@ def main():
         row(1, "1 | 1e7 u64, shuffled", " (L2-resident)"),
     ])
     p3, p5 = d3["partition_passes"], d5["partition_passes"]
-    passes = (f"Per-pass rooflines of the partitioned path (bench.py `partition_passes`, live CUDA events):\n"
-              f"config 3 bin {p3['bin']['ms']:.2f} ms ({p3['bin']['frac']:.2f} of HBM), query {p3['query']['ms']:.2f} ms\n"
-              f"({p3['query']['frac']:.2f} of the L2 gather rate), unbin {p3['unbin']['ms']:.2f} ms ({p3['unbin']['frac']:.2f} of HBM);\n"
-              f"config 5 bin {p5['bin']['ms']:.2f} ms, query {p5['query']['ms']:.2f} ms, unbin {p5['unbin']['ms']:.2f} ms. "
-              f"Clock throttle reasons seen: config 3 {d3['clocks']['reasons'] or 'none'}, config 5 "
-              f"{d5['clocks']['reasons'] or 'none'} (sw_power_cap is kept, as the rules allow).\n")
+    passes = (f"Per-pass rooflines of the partitioned path (bench.py `partition_passes`, CUDA events between the\n"
+              f"passes in a separate loop): config 3 bin {p3['bin']['ms']:.2f} ms ({p3['bin']['frac']:.2f} of HBM), "
+              f"query {p3['query']['ms']:.2f} ms\n({p3['query']['frac']:.2f} of the same-traffic port microbenchmark, "
+              f"{p3['query']['frac_vs_gather_only']:.2f} of the gather-only rate), unbin {p3['unbin']['ms']:.2f} ms "
+              f"({p3['unbin']['frac']:.2f} of HBM);\nconfig 5 bin {p5['bin']['ms']:.2f} ms, query {p5['query']['ms']:.2f} ms, "
+              f"unbin {p5['unbin']['ms']:.2f} ms. Clocks: config 3 median {d3['clocks']['sm_mhz']} MHz, minimum "
+              f"{d3['clocks'].get('sm_min_mhz')} MHz, reasons {d3['clocks']['reasons'] or 'none'} "
+              f"(`sw_power_cap` in {100 * d3['clocks'].get('sw_power_cap_share', 0):.0f} % of the samples; it is kept, "
+              f"as the rules allow).\n")
     p = os.path.join(ROOT, "DESIGN.md")
     s = open(p).read()
     a = s.index("| **3 (headline)** |")
@@ -58,10 +69,11 @@ def main():
 
     p = os.path.join(ROOT, "README.md")
     lines = open(p).read().split("\n")
+    k3 = d3["dominant_kernel"]
     rows = {
         "| config 3:": f"| config 3: 1e9 u64 keys, shuffled (partitioned path) | {v:.1f} Gkeys/s ({d3['ms_per_step']:.1f} ms), "
-                       f"{d3['gather_roofline']['frac']:.2f}× the measured gather roofline, {d3['roofline']['frac']:.2f} of HBM | "
-                       f"{e:.2f} Gkeys/s (PCIe-bound) | {c:.2f} Gkeys/s |",
+                       f"{d3['roofline']['frac']:.2f} of HBM on its own 40 B/key; dominant pass at {k3['frac']:.2f} of its "
+                       f"request-port bound | {e:.2f} Gkeys/s (PCIe-bound) | {c:.2f} Gkeys/s |",
         "| config 5:": f"| config 5: 1e9 k-mers, fused front end (partitioned path) | {d5['value']:.1f} Gkeys/s | "
                        f"{d5['e2e']['value']:.1f} Gkeys/s | {d5['cpu_baseline']['value']:.2f} Gkeys/s |",
         "| config 4:": f"| config 4: 3e8 strings | {d[4]['value']:.1f} Gkeys/s | {d[4]['e2e']['value']:.2f} Gkeys/s | "

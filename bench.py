@@ -763,6 +763,24 @@ def run_ours(args, cfg):
                     "frac": round(g_s / (r_port or r_gather), 4),
                     "gather_only_peak_gsectors_s": round(r_gather, 2),
                     "frac_vs_gather_only": round(g_s / r_gather, 4)}
+    elif cfg["kind"] == "str":
+        # The string kernel is bound by the SM's L1 data pipe: one wavefront per
+        # cycle per SM. Wavefronts per key come from the committed ncu capture of this kernel on
+        # this fixture (profiles/r02_traffic.json); the time and the clock are this run's.
+        wf = lsu_wavefronts("config4", "k_query_bytes")
+        clk = sampler.summary().get("sm_mhz")
+        if wf and clk:
+            sms_n = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            per_key = wf * sms_n / cfg["n"]
+            rate = nq * per_key / (step_ms * 1e-3) / (sms_n * clk * 1e6)
+            dominant = {"kernel": "k_query_bytes", "ms": round(step_ms, 4),
+                        "bound": "L1 data pipe: shared-memory T-table reads (16 per AES round) and the "
+                                 "per-lane key-byte loads, one wavefront per cycle per SM",
+                        "wavefronts_per_key": round(per_key, 3),
+                        "wavefronts_source": "ncu l1tex__data_pipe_lsu_wavefronts of this kernel on this "
+                                             "fixture (profiles/r02_ncu_full_query_config4_raw.csv)",
+                        "achieved_wavefronts_per_clk_per_sm": round(rate, 4), "peak": 1.0,
+                        "sm_mhz": clk, "frac": round(rate, 4)}
     res = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -835,6 +853,15 @@ def ph_gpu_trim_all():
     gc.collect()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
+
+
+def lsu_wavefronts(config_key: str, kernel: str):
+    """L1 data-pipe wavefronts per SM of `kernel` from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+            return json.load(f)[config_key]["kernels"][kernel].get("lsu_wavefronts_per_sm")
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def measured_traffic(config: int):

@@ -766,10 +766,11 @@ size_t search_smem_bytes(uint64_t S) {
     return ((sizeof(Shared) + 15) & ~size_t{15}) + ((S + 31) / 32) * 4;
 }
 
-// Can the kernel take this shape (the bitmap must fit in shared memory twice per SM)?
+// Can the kernel take this shape? The occupancy bitmap must fit in one CTA's shared memory
+// (S <= ~1.7 M slots per part; up to ~830 k, config 3's 762 k included, two CTAs share an SM).
 bool search_parts_supported(uint64_t S, uint64_t B, uint64_t max_part) {
     return S >= 1 && S < (1ull << 31) && B < (1ull << 31) && max_part < (1ull << 31) &&
-           search_smem_bytes(S) <= 112 * 1024;
+           search_smem_bytes(S) <= 216 * 1024;
 }
 
 // Searches every part. d_hashes / d_off: build_prepare_u64's output. d_pilots: P*B bytes.

@@ -268,3 +268,46 @@ def test_gpu_sort_skewed_hash_sets(ref, kind):
     assert st == want_st
     assert np.array_equal(got_h.cpu().numpy().view(np.uint64), want_h), kind
     assert np.array_equal(got_off.cpu().numpy().view(np.uint64), want_off), kind
+
+@pytest.mark.gpu
+def test_gpu_search_random_shapes_match_host_search():
+    """Seeded sweep over key counts, lambda, alpha, bucket functions, reduce kinds and forced
+    shapes (tiny S: the 64-bit mod; pow2 S; few buckets: big buckets and big-bucket evictions;
+    tight shapes: many evictions, reseeds and failures): the GPU search and the host search give
+    the same bytes or fail with the same code."""
+    _cuda()
+    ph = _ph()
+    rng = np.random.default_rng(20260)
+    fns = ["linear", "quadratic", "cubic", "skewed", "optimal"]
+    ran = unsupported = failed = 0
+    try:
+        for case in range(40):
+            n = int(rng.choice([700, 5_000, 40_000, 150_000]))
+            keys = corpus_u64_np(0, n, 500 + case)
+            kw = dict(bucket_fn=str(rng.choice(fns)), lambda_=(int(rng.integers(12, 60)), 10),
+                      alpha=(int(rng.integers(90, 100)), 100), retries=3,
+                      reduce=str(rng.choice(["fastmod-multi", "pow2-mul"])),
+                      remap=str(rng.choice(["plain32", "elias-fano"])))
+            if case % 3 == 0:  # a forced shape: P parts, S slots, B buckets
+                P = int(rng.choice([1, 3, 7]))
+                S = int(n / P * rng.uniform(1.02, 1.3)) + 8
+                if kw["reduce"] == "pow2-mul":
+                    S = 1 << int(np.ceil(np.log2(S)))
+                B = max(1, int(n / P / rng.uniform(1.5, 40.0)))
+                kw["shape"] = (P, S, B)
+            res = []
+            for mode in (1, 2):
+                ph.set_build_search(mode)
+                try:
+                    res.append(("ok", ph.build_u64(keys, ph.build_params("default", **kw))))
+                except ph.PhGpuError as e:
+                    res.append(("err", e.code))
+            if res[1] == ("err", ph.E_UNSUPPORTED):
+                unsupported += 1
+                continue
+            assert res[0] == res[1], (case, n, kw, res[0][0], res[1][0])
+            ran += 1
+            failed += res[0][0] == "err"
+    finally:
+        ph.set_build_search(0)
+    assert ran >= 25 and ran - failed >= 15, (ran, failed, unsupported)

@@ -27,6 +27,8 @@ def main():
         k = x.get("dominant_kernel")
         if not k:
             return "— (L1 data pipe, §3)"
+        if "frac_vs_gather_only" not in k:  # strings: the L1 data pipe
+            return f"{k['frac']:.2f} of the L1 data pipe"
         return f"{k['frac']:.2f} ({k['frac_vs_gather_only']:.2f})"
 
     def row(c, label, extra=""):

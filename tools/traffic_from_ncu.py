@@ -45,7 +45,10 @@ def main():
             continue
         rd = float(r[col["dram__bytes_read.sum"]]) * UNITS[units[col["dram__bytes_read.sum"]]]
         wr = float(r[col["dram__bytes_write.sum"]]) * UNITS[units[col["dram__bytes_write.sum"]]]
+        wf_col = "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg"
+        wf = float(r[hdr.index(wf_col)]) if wf_col in hdr and r[hdr.index(wf_col)] else None
         per[k] = {"dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
+                  "lsu_wavefronts_per_sm": wf,  # L1 data-pipe wavefronts, average per SM
                   "ncu_ms": float(r[col["gpu__time_duration.sum"]]) *
                   (1e-3 if units[col["gpu__time_duration.sum"]] == "usecond" else 1.0)}
     missing = [k for k in want if k not in per]

@@ -281,11 +281,11 @@ def test_gpu_search_random_shapes_match_host_search():
     fns = ["linear", "quadratic", "cubic", "skewed", "optimal"]
     ran = unsupported = failed = 0
     try:
-        for case in range(40):
+        for case in range(30):
             n = int(rng.choice([700, 5_000, 40_000, 150_000]))
             keys = corpus_u64_np(0, n, 500 + case)
             kw = dict(bucket_fn=str(rng.choice(fns)), lambda_=(int(rng.integers(12, 60)), 10),
-                      alpha=(int(rng.integers(90, 100)), 100), retries=3,
+                      alpha=(int(rng.integers(90, 100)), 100), retries=1,
                       reduce=str(rng.choice(["fastmod-multi", "pow2-mul"])),
                       remap=str(rng.choice(["plain32", "elias-fano"])))
             if case % 3 == 0:  # a forced shape: P parts, S slots, B buckets
@@ -310,4 +310,4 @@ def test_gpu_search_random_shapes_match_host_search():
             failed += res[0][0] == "err"
     finally:
         ph.set_build_search(0)
-    assert ran >= 25 and ran - failed >= 15, (ran, failed, unsupported)
+    assert ran >= 20 and ran - failed >= 12, (ran, failed, unsupported)

@@ -191,6 +191,55 @@ __global__ void __launch_bounds__(256, 4) k_port(const uint8_t* __restrict__ buf
     if (acc == 0x7fffffffu) *sink = acc;
 }
 
+// The same as k_port<1, 4>, but each warp stages its 256 four-byte outputs in shared memory
+// and lane 0 sends them with one 1 KiB bulk store (cp.async.bulk.global.shared::cta), double
+// buffered: does the TMA store path load the SM's request port less than per-thread stores?
+__global__ void __launch_bounds__(256, 4) k_port_bulk(const uint8_t* __restrict__ buf, uint64_t F,
+                                                      uint64_t nloads, uint64_t seed,
+                                                      const uint64_t* __restrict__ sin,
+                                                      uint32_t* __restrict__ sout, uint32_t* sink) {
+    __shared__ __align__(128) uint32_t stage[8][2][256];
+    uint64_t pk, pc;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pk));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pc));
+    const unsigned lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t it = 0;
+    for (uint64_t base = warp * 256; base + 256 <= nloads; base += nwarps * 256, it++) {
+        uint64_t kv[8];
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+                         : "=l"(kv[j]) : "l"(sin + base + j * 32 + lane), "l"(pc));
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t r = mix64(seed + (base + j * 32 + lane) * kGolden + (kv[j] & 1));
+            uint16_t x;
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+                         : "=h"(x) : "l"(buf + __umul64hi(r, F)), "l"(pk));
+            v[j] = x;
+        }
+        uint32_t* st = stage[wq][it & 1];
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer free
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; j++) st[j * 32 + lane] = v[j] + (uint32_t)kv[j];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                             sout + base),
+                         "r"((uint32_t)__cvta_generic_to_shared(st)), "r"(1024u), "l"(pc)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (sink == nullptr) return;
+}
+
 // Uniform random gather with a selectable load flavour (DRAM fetch-size experiments).
 template <int MODE>
 __device__ __forceinline__ uint16_t ld_mode(const uint8_t* p, uint64_t pol) {
@@ -482,6 +531,10 @@ int phb_port_model(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t s
     if (in_words == I && out_bytes == O) {                                                   \
         k_port<I, O><<<sms * 4, 256, 0, s>>>(d_buf, F, nloads, seed, d_sin, d_sout, d_sink); \
         return (int)cudaGetLastError();                                                      \
+    }
+    if (in_words == 1 && out_bytes == -4) {  // 4 B out through shared memory + bulk stores
+        k_port_bulk<<<sms * 4, 256, 0, s>>>(d_buf, F, nloads, seed, d_sin, (uint32_t*)d_sout, d_sink);
+        return (int)cudaGetLastError();
     }
     PH_PORT(0, 0) PH_PORT(1, 0) PH_PORT(2, 0) PH_PORT(0, 4) PH_PORT(1, 4) PH_PORT(1, 8) PH_PORT(2, 4) PH_PORT(2, 8)
 #undef PH_PORT

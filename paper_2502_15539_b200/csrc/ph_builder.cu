@@ -665,27 +665,34 @@ bool place_all(const Arith& a, uint64_t seed, const uint64_t* off, PartFeed& fee
     return true;
 }
 
-std::vector<uint8_t> finish(const Shape& sh, const ph_build_params& p, uint64_t seed,
-                            const std::vector<uint8_t>& pilots, const std::vector<PartResult>& parts,
-                            ph_build_stats* stats) {
-    const auto t0 = std::chrono::steady_clock::now();
+// The remap table's payload from the parts' free / overflow slot lists (engine.hpp:544-557).
+int remap_stage(const Shape& sh, const ph_build_params& p, const std::vector<PartResult>& parts,
+                std::vector<uint8_t>& payload, ph_build_stats* stats) {
     std::vector<uint64_t> fr, ov;
     for (const auto& r : parts) {
         fr.insert(fr.end(), r.free_slots.begin(), r.free_slots.end());
         ov.insert(ov.end(), r.overflow_slots.begin(), r.overflow_slots.end());
     }
     const std::vector<uint64_t> v = remap_values(fr, ov, sh.n, sh.P * sh.S);
-    std::vector<uint8_t> payload;
     bool fell_back = false;
     const int kind = remap_payload(p.remap_kind, v, sh.n, payload, &fell_back);
-    std::vector<uint8_t> out = ptrh_bytes(sh, p, seed, kind, pilots, payload);
     if (stats) {
         stats->remap_kind = (uint8_t)kind;
         stats->remap_fell_back = fell_back;
-        stats->pilot_bytes = pilots.size();
+        stats->pilot_bytes = sh.P * sh.B;
         stats->remap_payload_bytes = payload.size();
-        stats->remap_ms = ms_since(t0);
     }
+    return kind;
+}
+
+std::vector<uint8_t> finish(const Shape& sh, const ph_build_params& p, uint64_t seed,
+                            const std::vector<uint8_t>& pilots, const std::vector<PartResult>& parts,
+                            ph_build_stats* stats) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<uint8_t> payload;
+    const int kind = remap_stage(sh, p, parts, payload, stats);
+    std::vector<uint8_t> out = ptrh_bytes(sh, p, seed, kind, pilots, payload);
+    if (stats) stats->remap_ms = ms_since(t0);
     return out;
 }
 
@@ -736,6 +743,54 @@ void results_from_bitmaps(const Shape& sh, const std::vector<uint32_t>& taken, u
             }
         });
     for (auto& t : ws) t.join();
+}
+
+// Host keys -> device. A plain cudaMemcpy from pageable memory runs at ~11 GB/s (0.7 s for
+// the 8 GB of config 3); here host threads copy 16 MiB pieces into their own pinned buffers
+// and send them with async copies, two buffers per thread, so the transfer runs at the PCIe
+// rate (the host memcpy of one piece overlaps the DMA of the previous ones).
+cudaError_t upload_pipelined(uint64_t* d, const uint64_t* h, size_t n, unsigned threads, int device) {
+    constexpr size_t kPiece = size_t{2} << 20;  // words: 16 MiB
+    if (n < 4 * kPiece) return cudaMemcpy(d, h, n * 8, cudaMemcpyHostToDevice);
+    const size_t pieces = (n + kPiece - 1) / kPiece;
+    const unsigned T = (unsigned)std::min<size_t>(std::min(8u, thread_count(threads)), pieces);
+    std::atomic<size_t> next{0};
+    std::atomic<int> err{(int)cudaSuccess};
+    std::vector<std::thread> ws;
+    for (unsigned t = 0; t < T; t++)
+        ws.emplace_back([&] {
+            auto fail = [&](cudaError_t e) {
+                int ok = (int)cudaSuccess;
+                if (e != cudaSuccess) err.compare_exchange_strong(ok, (int)e);
+                return e != cudaSuccess;
+            };
+            if (fail(cudaSetDevice(device))) return;
+            uint64_t* pin[2] = {nullptr, nullptr};
+            cudaStream_t st = nullptr;
+            cudaEvent_t ev[2] = {nullptr, nullptr};
+            bool ok = !fail(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            for (int b = 0; b < 2 && ok; b++)
+                ok = !fail(cudaHostAlloc(reinterpret_cast<void**>(&pin[b]), kPiece * 8, cudaHostAllocDefault)) &&
+                     !fail(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+            for (size_t k = 0; ok && err.load() == (int)cudaSuccess; k++) {
+                const size_t i = next.fetch_add(1);
+                if (i >= pieces) break;
+                const int b = (int)(k & 1);
+                const size_t w0 = i * kPiece, len = std::min(kPiece, n - w0);
+                if (k >= 2 && fail(cudaEventSynchronize(ev[b]))) break;
+                std::memcpy(pin[b], h + w0, len * 8);
+                if (fail(cudaMemcpyAsync(d + w0, pin[b], len * 8, cudaMemcpyHostToDevice, st))) break;
+                if (fail(cudaEventRecord(ev[b], st))) break;
+            }
+            if (st) fail(cudaStreamSynchronize(st));
+            for (int b = 0; b < 2; b++) {
+                if (ev[b]) cudaEventDestroy(ev[b]);
+                if (pin[b]) cudaFreeHost(pin[b]);
+            }
+            if (st) cudaStreamDestroy(st);
+        });
+    for (auto& t : ws) t.join();
+    return (cudaError_t)err.load();
 }
 
 Shape resolve_shape(uint64_t n, const ph_build_params& p) {
@@ -889,7 +944,7 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
         const uint64_t* dk = keys;
         if (!is_device_ptr(keys)) {
             cuda(cudaMalloc(&d_keys, n * 8), "device key buffer");
-            cuda(cudaMemcpy(d_keys, keys, n * 8, cudaMemcpyHostToDevice), "key upload");
+            cuda(upload_pipelined(d_keys, keys, n, threads, device), "key upload");
             dk = d_keys;
         }
         cuda(cudaMalloc(&d_h, n * 8), "device hash buffer");
@@ -953,9 +1008,7 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                     if (!hst[1]) {
                         searched = true;
                         if (!hst[0]) {  // every part placed
-                            std::vector<uint8_t> pilots(sh.P * sh.B);
                             std::vector<uint32_t> taken(sh.P * (uint64_t)words);
-                            cuda(cudaMemcpy(pilots.data(), d_pilots, pilots.size(), cudaMemcpyDeviceToHost), "pilots");
                             cuda(cudaMemcpy(taken.data(), d_taken, taken.size() * 4, cudaMemcpyDeviceToHost),
                                  "occupancy bitmaps");
                             const double t_copy = ms_since(tp);
@@ -963,10 +1016,30 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                             results_from_bitmaps(sh, taken, words, threads, parts);
                             if (trace)
                                 std::fprintf(stderr, "[ph_gpu build] search: alloc %.1f ms, kernel+workspace %.1f ms, "
-                                             "copy back %.1f ms, slot lists %.1f ms\n", t_alloc, t_kernel - t_alloc,
+                                             "bitmaps back %.1f ms, slot lists %.1f ms\n", t_alloc, t_kernel - t_alloc,
                                              t_copy - t_kernel, ms_since(tp) - t_copy);
                             search_ms += ms_since(tp);
-                            const std::vector<uint8_t> out = finish(sh, *params, seed, pilots, parts, stats);
+                            // the remap table, then the PTRH bytes assembled in the returned
+                            // buffer itself: the pilots come straight from the device
+                            const auto tr = std::chrono::steady_clock::now();
+                            std::vector<uint8_t> payload;
+                            const int kind = remap_stage(sh, *params, parts, payload, stats);
+                            const std::vector<uint8_t> head = ptrh_bytes(sh, *params, seed, kind, {}, {});
+                            const uint64_t pb = sh.P * sh.B;
+                            std::vector<uint8_t> hdr(head);  // sizes of the empty sections -> real ones
+                            std::memcpy(hdr.data() + 56, &pb, 8);
+                            const uint64_t rl = payload.size();
+                            std::memcpy(hdr.data() + 64, &rl, 8);
+                            uint8_t* buf = static_cast<uint8_t*>(std::malloc(hdr.size() + pb + rl));
+                            if (!buf) throw std::bad_alloc();
+                            std::memcpy(buf, hdr.data(), hdr.size());
+                            const cudaError_t ce = cudaMemcpy(buf + hdr.size(), d_pilots, pb, cudaMemcpyDeviceToHost);
+                            if (ce != cudaSuccess) {
+                                std::free(buf);
+                                cuda(ce, "pilots");
+                            }
+                            std::memcpy(buf + hdr.size() + pb, payload.data(), rl);
+                            if (stats) stats->remap_ms = ms_since(tr);
                             if (stats) {
                                 stats->n = n, stats->parts = sh.P, stats->slots_per_part = sh.S;
                                 stats->buckets_per_part = sh.B, stats->seed = seed, stats->attempts = attempt + 1;
@@ -976,8 +1049,8 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                                 stats->search_ms = search_ms, stats->total_ms = ms_since(t0);
                                 stats->reserved[0] = 1;  // the search ran on the GPU
                             }
-                            if (!(*ptrh = to_malloc(out))) throw std::bad_alloc();
-                            *len = out.size();
+                            *ptrh = buf;
+                            *len = hdr.size() + pb + rl;
                             return PH_OK;
                         }
                         search_ms += ms_since(tp);  // a part failed: reseed

@@ -13,10 +13,14 @@
 //   prologue   bucket boundaries of the part's sorted hashes (exact gamma), the visiting
 //              order by a stable counting sort on bucket size, and the part's hashes copied
 //              into visiting order, so the main loop streams them;
-//   step       thread p hashes the bucket's keys with pilot p and tests the part's occupancy
-//              bitmap, which lives in shared memory (S bits); ballot + cross-warp minimum
-//              pick the smallest free pilot; that thread marks the slots. Two CTA barriers
-//              per bucket, no global-memory round trip on the common path;
+//   step       eight buckets at once, one per warp: lane p of a round hashes the bucket's keys
+//              with pilot 32*round + p and tests the part's occupancy bitmap, which lives in
+//              shared memory (S bits); the first round with a free pilot ends the warp's
+//              search; the eight winners commit in visiting order (a claim per slot, rolled
+//              back and redone serially if two buckets of the batch want one slot). Two CTA
+//              barriers per eight buckets, no global-memory round trip on the common path;
+//   full step  (an evicted bucket pending, or no pilot free) all 256 pilots of one bucket,
+//              one per thread;
 //   eviction   (0.6 % of buckets at lambda = 3) every thread prices its pilot from the
 //              global owner[] array, a block argmin picks the cheapest, thread 0 displaces
 //              the hit buckets exactly in the reference's order and pushes them on a small
@@ -335,15 +339,14 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                 cend = sm.cbeg[kcur] + sm.cnt[kcur];  // (kept in a register between steps)
             }
             if (!single && hn == 0 && cursor >= nbig && cursor < nonempty) {
-                // Batch mode (no evicted bucket pending): the next 8 / wpb buckets at once,
-                // wpb warps (32 * wpb pilots) per bucket, each against the bitmap as it
-                // stands. They commit in visiting order; a bucket commits if its pilot's
-                // slots are still free after the earlier commits of the batch (bits are only
-                // set here, so no smaller pilot can have become free: the choice is the
-                // sequential search's). A bucket that lost a slot restarts the next batch; one
-                // that found no pilot doubles wpb, and at 256 pilots goes to the full step
-                // below (an eviction). Batches whose winners sit in the lower half of their
-                // pilot range halve wpb.
+                // Batch mode (no evicted bucket pending): the next eight buckets at once, one per
+                // warp. A warp tests its bucket's pilots 32 at a time, smallest first, against
+                // the bitmap as it stands, until one is free (eight rounds cover all 256). The
+                // buckets commit in visiting order; a bucket commits if its pilot's slots are
+                // still free after the earlier commits of the batch (bits are only set here, so
+                // no smaller pilot can have become free: the choice is the sequential search's).
+                // A bucket that lost a slot restarts the next batch; one with no free pilot at
+                // all goes to the full step below (an eviction).
                 const long long t_b0 = clock64();
                 const uint32_t nb = min(8u / wpb, nonempty - cursor);
                 const uint32_t q = warp / wpb, c = cursor + q;
@@ -353,10 +356,12 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                         while (c >= sm.cbeg[kc] + sm.cnt[kc]) kc--;
                     mybk = w.ord[c];
                     const uint64_t* kq = w.hre + sm.cpos[kc] + (uint64_t)(c - sm.cbeg[kc]) * kc;
-                    const uint32_t pil = (warp % wpb) * 32 + lane;
+                    uint32_t win = 32, round = 0;
+                    uint32_t r8[kRegK];
+                    for (; round < 8; round++) {  // 32 pilots per round, smallest first
+                    const uint32_t pil = round * 32 + lane;
                     const uint64_t hl = kC * ((uint64_t)pil ^ a.seed);
                     bool ok = true;
-                    uint32_t r8[kRegK];
                     if (kc <= 2) {  // (warp-uniform: the bucket is the warp's)
                         uint32_t r2[2];
                         ok = test_pilot_reg<2>(a, taken, kq, kc, hl, r2);
@@ -379,7 +384,6 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                         }
                     }
                     const unsigned bal = __ballot_sync(kFull, ok);
-                    uint32_t win;
                     if (kc <= kRegK) {
                         win = bal ? (uint32_t)__ffs(bal) - 1 : 32u;
                         if (lane == win) {
@@ -390,8 +394,10 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                     } else {
                         win = first_distinct(bal, sl, kc, sm.bsl[warp], lane);
                     }
+                    if (win < 32) break;
+                    }
                     if (lane == 0) {
-                        sm.bwin[warp] = win < 32 ? (warp % wpb) * 32 + win : 256u;
+                        sm.bwin[warp] = win < 32 ? round * 32 + win : 256u;
                         sm.bkc[warp] = kc;
                     }
                     if (tid == 0) {
@@ -464,12 +470,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                     if (lane == 0) pl[mybk] = (uint8_t)sm.bwin[warp];
                 }
                 cursor += nc;
-                if (why == 1) {
-                    if (wpb == 8) single = true;
-                    else wpb *= 2;
-                } else if (why == 0 && (sm.ncommit >> 16) && wpb > 1) {
-                    wpb /= 2;
-                }
+                if (why == 1) single = true;  // none of the 256 pilots is free: an eviction
                 if (sm.flags) {
                     failed = true;
                     break;

@@ -756,22 +756,26 @@ cudaError_t upload_pipelined(uint64_t* d, const uint64_t* h, size_t n, unsigned 
     const unsigned T = (unsigned)std::min<size_t>(std::min(8u, thread_count(threads)), pieces);
     std::atomic<size_t> next{0};
     std::atomic<int> err{(int)cudaSuccess};
+    uint64_t* pin_all = nullptr;  // one page-locked region, two pieces per thread
+    cudaError_t ea = cudaHostAlloc(reinterpret_cast<void**>(&pin_all), (size_t)T * 2 * kPiece * 8, cudaHostAllocDefault);
+    if (ea != cudaSuccess) {
+        cudaGetLastError();
+        return cudaMemcpy(d, h, n * 8, cudaMemcpyHostToDevice);
+    }
     std::vector<std::thread> ws;
     for (unsigned t = 0; t < T; t++)
-        ws.emplace_back([&] {
+        ws.emplace_back([&, t] {
             auto fail = [&](cudaError_t e) {
                 int ok = (int)cudaSuccess;
                 if (e != cudaSuccess) err.compare_exchange_strong(ok, (int)e);
                 return e != cudaSuccess;
             };
             if (fail(cudaSetDevice(device))) return;
-            uint64_t* pin[2] = {nullptr, nullptr};
+            uint64_t* pin[2] = {pin_all + (size_t)t * 2 * kPiece, pin_all + ((size_t)t * 2 + 1) * kPiece};
             cudaStream_t st = nullptr;
             cudaEvent_t ev[2] = {nullptr, nullptr};
             bool ok = !fail(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-            for (int b = 0; b < 2 && ok; b++)
-                ok = !fail(cudaHostAlloc(reinterpret_cast<void**>(&pin[b]), kPiece * 8, cudaHostAllocDefault)) &&
-                     !fail(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+            for (int b = 0; b < 2 && ok; b++) ok = !fail(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
             for (size_t k = 0; ok && err.load() == (int)cudaSuccess; k++) {
                 const size_t i = next.fetch_add(1);
                 if (i >= pieces) break;
@@ -783,13 +787,12 @@ cudaError_t upload_pipelined(uint64_t* d, const uint64_t* h, size_t n, unsigned 
                 if (fail(cudaEventRecord(ev[b], st))) break;
             }
             if (st) fail(cudaStreamSynchronize(st));
-            for (int b = 0; b < 2; b++) {
+            for (int b = 0; b < 2; b++)
                 if (ev[b]) cudaEventDestroy(ev[b]);
-                if (pin[b]) cudaFreeHost(pin[b]);
-            }
             if (st) cudaStreamDestroy(st);
         });
     for (auto& t : ws) t.join();
+    cudaFreeHost(pin_all);
     return (cudaError_t)err.load();
 }
 
@@ -944,7 +947,11 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
         const uint64_t* dk = keys;
         if (!is_device_ptr(keys)) {
             cuda(cudaMalloc(&d_keys, n * 8), "device key buffer");
+            const double t_m = ms_since(t0);
             cuda(upload_pipelined(d_keys, keys, n, threads, device), "key upload");
+            if (std::getenv("PH_GPU_BUILD_TRACE"))
+                std::fprintf(stderr, "[ph_gpu build] key buffer cudaMalloc %.1f ms, upload %.1f ms\n", t_m,
+                             ms_since(t0) - t_m);
             dk = d_keys;
         }
         cuda(cudaMalloc(&d_h, n * 8), "device hash buffer");

@@ -6,6 +6,8 @@
 //   uint64_t index_no_remap(uint64_t) / index_no_remap(std::string_view) index.hpp:60-61
 //   void index_loop / index_batched / index_stream(span keys, ..., uint64_t* out, bool minimal)
 //                                                                       index.hpp:72-81
+// and, for u64 keys, ph_gpu::build(keys, params) for build() + serialize()
+// (construction.cpp:113-143): the same PTRH bytes, built on the GPU.
 //
 // Host spans are staged through the library's pipelined H2D -> kernel -> D2H
 // path; the call returns when `out` is complete, like the reference. The
@@ -152,5 +154,30 @@ class PtrHashIndex {
     ph_gpu_index* h_ = nullptr;
     ph_gpu_info info_{};
 };
+
+// ---- construction (u64 keys) ------------------------------------------------------------
+// preset() (shape.cpp:65-84): "fast", "default" or "compact".
+inline ph_build_params preset(const char* name) {
+    ph_build_params p{};
+    check(ph_build_preset(name, &p));
+    return p;
+}
+
+// build(std::span<const uint64_t>, params, threads, stats) + serialize()
+// (/root/reference/proj/src/construction.cpp:113-143, src/serde.cpp:142-174): the PTRH v1
+// bytes of the index over the distinct keys, the same bytes the reference produces. Hashing,
+// sorting and the per-part pilot search run on `device`; `keys` may be host or device memory.
+// Throws Error with PH_E_DUPLICATE (BuildError kDuplicateKeys), PH_E_BUILD_FAILED (kFailed)
+// or PH_E_INVALID (kInvalid), build.hpp:48-60.
+inline std::vector<uint8_t> build(std::span<const uint64_t> keys, const ph_build_params& params,
+                                  unsigned threads = 0, int device = 0,
+                                  ph_build_stats* stats = nullptr) {
+    uint8_t* bytes = nullptr;
+    size_t len = 0;
+    check(ph_gpu_build_u64(keys.data(), keys.size(), &params, threads, device, &bytes, &len, stats));
+    std::vector<uint8_t> out(bytes, bytes + len);
+    ph_free(bytes);
+    return out;
+}
 
 }  // namespace ph_gpu

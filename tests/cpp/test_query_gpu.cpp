@@ -112,6 +112,33 @@ int main(int argc, char** argv) {
     sym(lib, "ref_corpus_u64", R.corpus_u64);
     sym(lib, "ref_free", R.free_);
 
+    // construction through the C++ wrapper: ph_gpu::build gives the reference's bytes for the
+    // same keys and preset (pilot search on the GPU and on host threads), and reports
+    // duplicate keys like the reference's BuildError::kDuplicateKeys
+    {
+        const auto keys = corpus(R, 150'000, 5);
+        for (const char* name : {"fast", "default", "compact"}) {
+            const auto want = build(R, keys, name);
+            for (const int mode : {2, 1}) {
+                CHECK(ph_gpu_set_build_search(mode) == PH_OK);
+                ph_build_stats st{};
+                const auto got = ph_gpu::build(keys, ph_gpu::preset(name), 0, 0, &st);
+                CHECK(got == want);
+                CHECK(st.n == keys.size() && (st.reserved[0] == 1) == (mode == 2));
+            }
+        }
+        CHECK(ph_gpu_set_build_search(0) == PH_OK);
+        auto dup = keys;
+        dup.back() = dup[3];
+        bool threw = false;
+        try {
+            ph_gpu::build(dup, ph_gpu::preset("default"));
+        } catch (const ph_gpu::Error& e) {
+            threw = e.code() == PH_E_DUPLICATE;
+        }
+        CHECK(threw);
+    }
+
     // test_query.cpp:23-49 — loop, batched and streaming agree elementwise, and
     // equal the reference, on a mix of member and non-member keys.
     {

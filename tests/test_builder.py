@@ -311,3 +311,23 @@ def test_gpu_search_random_shapes_match_host_search():
     finally:
         ph.set_build_search(0)
     assert ran >= 20 and ran - failed >= 12, (ran, failed, unsupported)
+
+@pytest.mark.gpu
+def test_gpu_search_falls_back_for_large_parts(ref):
+    """A part whose occupancy bitmap does not fit one CTA's shared memory (S = 2e6 slots) is
+    searched on host threads in the default mode (same bytes as the reference) and refused
+    with E_UNSUPPORTED when the GPU search is forced."""
+    _cuda()
+    ph = _ph()
+    keys = corpus_u64_np(0, 60_000, 77)
+    shape = (1, 2_000_000, 20_000)
+    want = ref.build_u64_shape(keys, ref.params("default", lambda_=(30, 10)), *shape)
+    got, st = ph.build_u64(keys, ph.build_params("default", lambda_=(30, 10), shape=shape), stats=True)
+    assert got == want and not st["search_on_gpu"]
+    ph.set_build_search(2)
+    try:
+        with pytest.raises(ph.PhGpuError) as e:
+            ph.build_u64(keys, ph.build_params("default", lambda_=(30, 10), shape=shape))
+        assert e.value.code == ph.E_UNSUPPORTED
+    finally:
+        ph.set_build_search(0)

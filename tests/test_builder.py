@@ -329,5 +329,10 @@ def test_gpu_search_falls_back_for_large_parts(ref):
         with pytest.raises(ph.PhGpuError) as e:
             ph.build_u64(keys, ph.build_params("default", lambda_=(30, 10), shape=shape))
         assert e.value.code == ph.E_UNSUPPORTED
+        # S = 1.2e6: the bitmap fits one CTA per SM (not two): still the GPU search, same bytes
+        shape1 = (1, 1_200_000, 20_000)
+        want1 = ref.build_u64_shape(keys, ref.params("default", lambda_=(30, 10)), *shape1)
+        got1, st1 = ph.build_u64(keys, ph.build_params("default", lambda_=(30, 10), shape=shape1), stats=True)
+        assert got1 == want1 and st1["search_on_gpu"]
     finally:
         ph.set_build_search(0)

@@ -189,7 +189,19 @@ int ph_build_compute_shape(uint64_t n, const ph_build_params* params, uint64_t* 
 int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* params,
                      unsigned threads, int device, uint8_t** ptrh, size_t* len,
                      ph_build_stats* stats);
-/* Where ph_gpu_build_u64 runs the per-part pilot search (engine.hpp:105-292): 0 (default) on
+/* build(std::span<const std::string>, params, threads, stats) + serialize()
+ * (construction.cpp:154-226) for keys given as concatenated bytes + offsets[n+1] (both host or
+ * both device): every key is hashed on `device` with the index's string hash (hash_algo: 1 =
+ * aes64, what the reference picks on an x86 host with AES-NI for n < 2^32, hash.cpp:40-46; 3 =
+ * portable64), and the 64-bit hashes go through the same sort and pilot search as a u64 build.
+ * The bytes equal the reference's build for the same keys, parameters and hash. Equal
+ * fingerprints (status of the sort) reseed once, as the reference does; a second time the
+ * reference widens to its 128-bit hash, which this builder does not produce: PH_E_UNSUPPORTED
+ * (so is n >= 2^32). Other errors as ph_gpu_build_u64. */
+int ph_gpu_build_bytes(const uint8_t* bytes, const uint64_t* offsets, size_t n,
+                       const ph_build_params* params, int hash_algo, unsigned threads, int device,
+                       uint8_t** ptrh, size_t* len, ph_build_stats* stats);
+/* Where ph_gpu_build_u64 / ph_gpu_build_bytes run the per-part pilot search (engine.hpp:105-292): 0 (default) on
  * the GPU, one CTA per part (csrc/ph_search.cu), falling back to host threads for shapes the
  * kernel does not take (slots_per_part beyond the shared-memory bitmap, a bucket over 64
  * keys); 1 always on host threads; 2 on the GPU or PH_E_UNSUPPORTED. Either way the bytes are

@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <queue>
 #include <stdexcept>
@@ -480,12 +481,14 @@ int remap_payload(int kind, const std::vector<uint64_t>& v, uint64_t n, std::vec
 // PTRH v1 (serde.hpp:12-31, serialize: serde.cpp:142-170)
 std::vector<uint8_t> ptrh_bytes(const Shape& sh, const ph_build_params& p, uint64_t seed,
                                 int remap_kind, const std::vector<uint8_t>& pilots,
-                                const std::vector<uint8_t>& remap) {
+                                const std::vector<uint8_t>& remap, uint8_t key_kind = 0,
+                                uint8_t hash_algo = 0) {
     std::vector<uint8_t> o;
     o.reserve(72 + pilots.size() + remap.size());
     o.insert(o.end(), {'P', 'T', 'R', 'H'});
     put32(o, 1);
-    o.insert(o.end(), {0 /*u64 keys*/, 0 /*fx64*/, p.bucket_fn, (uint8_t)remap_kind, p.reduce_kind, 0, 0, 0});
+    o.insert(o.end(), {key_kind /*0 u64, 1 bytes*/, hash_algo /*0 fx64, 1 aes64, 3 portable64*/, p.bucket_fn,
+                       (uint8_t)remap_kind, p.reduce_kind, 0, 0, 0});
     for (uint64_t x : {sh.n, sh.P, sh.S, sh.B, seed, (uint64_t)pilots.size(), (uint64_t)remap.size()})
         put64(o, x);
     o.insert(o.end(), pilots.begin(), pilots.end());
@@ -687,11 +690,11 @@ int remap_stage(const Shape& sh, const ph_build_params& p, const std::vector<Par
 
 std::vector<uint8_t> finish(const Shape& sh, const ph_build_params& p, uint64_t seed,
                             const std::vector<uint8_t>& pilots, const std::vector<PartResult>& parts,
-                            ph_build_stats* stats) {
+                            ph_build_stats* stats, uint8_t key_kind = 0, uint8_t hash_algo = 0) {
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<uint8_t> payload;
     const int kind = remap_stage(sh, p, parts, payload, stats);
-    std::vector<uint8_t> out = ptrh_bytes(sh, p, seed, kind, pilots, payload);
+    std::vector<uint8_t> out = ptrh_bytes(sh, p, seed, kind, pilots, payload, key_kind, hash_algo);
     if (stats) stats->remap_ms = ms_since(t0);
     return out;
 }
@@ -915,11 +918,23 @@ int ph_build_from_sorted_u64(const uint64_t* hashes, const uint64_t* offsets, si
     });
 }
 
-int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* params,
-                     unsigned threads, int device, uint8_t** ptrh, size_t* len,
-                     ph_build_stats* stats) {
-    PH_RANGE("ph_gpu_build_u64");
-    if ((!keys && n) || !params || !ptrh || !len) return phg::report_error(PH_E_INVALID, "null argument");
+}  // extern "C"
+
+namespace {
+// What differs between key kinds in a build: where the attempt's u64 keys come from (u64
+// keys: the input itself; byte strings: per seed, the pre-images key' with
+// C * (key' ^ seed) == hash_bytes(key, seed).lo, so that the u64 front reproduces the string
+// hashes), the header's key kind and hash id, and what equal hashes mean.
+struct KeyFeed {
+    uint8_t key_kind = 0, hash_algo = 0;
+    bool dup_is_error = true;  // u64: equal hashes are equal keys (construction.cpp:128-133)
+    // host -> device staging before the attempts; returns the time it took in upload_ms
+    std::function<void(unsigned threads, int device)> upload;
+    std::function<const uint64_t*(uint64_t seed, int sms)> keys_for_seed;
+};
+
+int build_impl(size_t n, const ph_build_params* params, unsigned threads, int device, KeyFeed& src,
+               uint8_t** ptrh, size_t* len, ph_build_stats* stats) {
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != device && cudaSetDevice(device) != cudaSuccess)
@@ -930,7 +945,6 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
             if (prev >= 0 && prev != dev) cudaSetDevice(prev);
         }
     } restore{prev, device};
-    uint64_t* d_keys = nullptr;
     uint64_t* d_h = nullptr;
     uint64_t* d_off = nullptr;
     const int rc = guarded([&] {
@@ -944,16 +958,8 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
             if (e == cudaErrorMemoryAllocation) throw BuildFail(PH_E_NOMEM, what);
             if (e != cudaSuccess) throw BuildFail(PH_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
         };
-        const uint64_t* dk = keys;
-        if (!is_device_ptr(keys)) {
-            cuda(cudaMalloc(&d_keys, n * 8), "device key buffer");
-            const double t_m = ms_since(t0);
-            cuda(upload_pipelined(d_keys, keys, n, threads, device), "key upload");
-            if (std::getenv("PH_GPU_BUILD_TRACE"))
-                std::fprintf(stderr, "[ph_gpu build] key buffer cudaMalloc %.1f ms, upload %.1f ms\n", t_m,
-                             ms_since(t0) - t_m);
-            dk = d_keys;
-        }
+        src.upload(threads, device);
+        uint32_t duplicate_failures = 0;
         cuda(cudaMalloc(&d_h, n * 8), "device hash buffer");
         cuda(cudaMalloc(&d_off, (sh.P + 1) * 8), "device offsets");
         int sms = 148;
@@ -967,10 +973,19 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
             PH_RANGE("build attempt");
             auto tp = std::chrono::steady_clock::now();
             int status = 0;
+            const uint64_t* dk = src.keys_for_seed(seed, sms);
             cuda(phg::build_prepare_u64(dk, n, sh.P, sh.S, seed, d_h, d_off, &status, nullptr, sms),
                  "build_prepare_u64");
             prep_ms += ms_since(tp);
-            if (status == 2) throw BuildFail(PH_E_DUPLICATE, "duplicate keys in input");
+            if (status == 2) {
+                if (src.dup_is_error) throw BuildFail(PH_E_DUPLICATE, "duplicate keys in input");
+                // byte strings (construction.cpp:208-216): equal keys or a fingerprint collision;
+                // the reference reseeds and, the second time, widens to the 128-bit hash
+                if (++duplicate_failures >= 2)
+                    throw BuildFail(PH_E_UNSUPPORTED,
+                                    "persistent duplicate 64-bit fingerprints (duplicate keys in input?): the "
+                                    "reference widens to its 128-bit hash here, which this builder does not produce");
+            }
             bool searched = false;
             if (status == 0 && g_search_mode.load() != 1) {
                 // the pilot search on the GPU (ph_search.cu): one CTA per part
@@ -1031,7 +1046,8 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                             const auto tr = std::chrono::steady_clock::now();
                             std::vector<uint8_t> payload;
                             const int kind = remap_stage(sh, *params, parts, payload, stats);
-                            const std::vector<uint8_t> head = ptrh_bytes(sh, *params, seed, kind, {}, {});
+                            const std::vector<uint8_t> head =
+                                ptrh_bytes(sh, *params, seed, kind, {}, {}, src.key_kind, src.hash_algo);
                             const uint64_t pb = sh.P * sh.B;
                             std::vector<uint8_t> hdr(head);  // sizes of the empty sections -> real ones
                             std::memcpy(hdr.data() + 56, &pb, 8);
@@ -1076,7 +1092,8 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                 search_ms += ms_since(tp);
                 if (feed.err != cudaSuccess) cuda(feed.err, "hash transfer");
                 if (ok) {
-                    const std::vector<uint8_t> out = finish(sh, *params, seed, pilots, parts, stats);
+                    const std::vector<uint8_t> out =
+                        finish(sh, *params, seed, pilots, parts, stats, src.key_kind, src.hash_algo);
                     if (stats) {
                         stats->n = n, stats->parts = sh.P, stats->slots_per_part = sh.S;
                         stats->buckets_per_part = sh.B, stats->seed = seed, stats->attempts = attempt + 1;
@@ -1096,9 +1113,108 @@ int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* para
                                                std::to_string(params->max_seed_retries + 1) +
                                                " seed attempts");
     });
-    if (d_keys) cudaFree(d_keys);
     if (d_h) cudaFree(d_h);
     if (d_off) cudaFree(d_off);
+    return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int ph_gpu_build_u64(const uint64_t* keys, size_t n, const ph_build_params* params,
+                     unsigned threads, int device, uint8_t** ptrh, size_t* len,
+                     ph_build_stats* stats) {
+    PH_RANGE("ph_gpu_build_u64");
+    if ((!keys && n) || !params || !ptrh || !len) return phg::report_error(PH_E_INVALID, "null argument");
+    uint64_t* d_keys = nullptr;
+    KeyFeed feed;
+    feed.upload = [&](unsigned th, int dev) {
+        if (is_device_ptr(keys) || !n) return;
+        const auto t0 = std::chrono::steady_clock::now();
+        cudaError_t e = cudaMalloc(&d_keys, n * 8);
+        if (e == cudaErrorMemoryAllocation) throw BuildFail(PH_E_NOMEM, "device key buffer");
+        const double t_m = ms_since(t0);
+        if (e == cudaSuccess) e = upload_pipelined(d_keys, keys, n, th, dev);
+        if (e != cudaSuccess) throw BuildFail(PH_E_CUDA, std::string("key upload: ") + cudaGetErrorString(e));
+        if (std::getenv("PH_GPU_BUILD_TRACE"))
+            std::fprintf(stderr, "[ph_gpu build] key buffer cudaMalloc %.1f ms, upload %.1f ms\n", t_m,
+                         ms_since(t0) - t_m);
+    };
+    feed.keys_for_seed = [&](uint64_t, int) { return d_keys ? d_keys : keys; };
+    const int rc = build_impl(n, params, threads, device, feed, ptrh, len, stats);
+    if (d_keys) cudaFree(d_keys);
+    return rc;
+}
+
+int ph_gpu_build_bytes(const uint8_t* bytes, const uint64_t* offsets, size_t n,
+                       const ph_build_params* params, int hash_algo, unsigned threads, int device,
+                       uint8_t** ptrh, size_t* len, ph_build_stats* stats) {
+    PH_RANGE("ph_gpu_build_bytes");
+    if (!offsets || !params || !ptrh || !len) return phg::report_error(PH_E_INVALID, "null argument");
+    if (hash_algo != 1 && hash_algo != 3)
+        return phg::report_error(PH_E_UNSUPPORTED, "string builds use the 64-bit hashes: aes64 (1) or portable64 (3)");
+    if (n >= (uint64_t{1} << 32))
+        return phg::report_error(PH_E_UNSUPPORTED, "2^32 or more string keys need the 128-bit hash");
+    uint8_t* d_bytes = nullptr;
+    uint64_t* d_offs = nullptr;
+    uint64_t* d_pk = nullptr;
+    const uint8_t* db = bytes;
+    const uint64_t* dof = offsets;
+    // the inverse of the integer hash's multiplier mod 2^64 (Newton iteration; C is odd)
+    uint64_t cinv = kMix;
+    for (int i = 0; i < 6; i++) cinv *= 2 - kMix * cinv;
+    KeyFeed feed;
+    feed.key_kind = 1;
+    feed.hash_algo = (uint8_t)hash_algo;
+    feed.dup_is_error = false;
+    feed.upload = [&](unsigned, int) {
+        auto cuda = [](cudaError_t e, const char* what) {
+            if (e == cudaErrorMemoryAllocation) throw BuildFail(PH_E_NOMEM, what);
+            if (e != cudaSuccess) throw BuildFail(PH_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        };
+        if (!is_device_ptr(offsets)) {
+            for (size_t i = 0; i < n; i++)
+                if (offsets[i + 1] < offsets[i]) throw BuildFail(PH_E_INVALID, "offsets must be non-decreasing");
+            const uint64_t total = offsets[n] - offsets[0];
+            if (total && !bytes) throw BuildFail(PH_E_INVALID, "null bytes");
+            if (is_device_ptr(bytes)) throw BuildFail(PH_E_INVALID, "bytes and offsets must both be host or both device");
+            cuda(cudaMalloc(&d_offs, (n + 1) * 8), "device offsets of the keys");
+            cuda(cudaMemcpy(d_offs, offsets, (n + 1) * 8, cudaMemcpyHostToDevice), "offset upload");
+            cuda(cudaMalloc(&d_bytes, total + 32), "device key bytes");
+            // offsets index `bytes`; the device copy starts at offsets[0]
+            cuda(cudaMemcpy(d_bytes, bytes + offsets[0], total, cudaMemcpyHostToDevice), "key byte upload");
+            db = d_bytes - offsets[0];
+            dof = d_offs;
+        } else if (!is_device_ptr(bytes)) {
+            throw BuildFail(PH_E_INVALID, "bytes and offsets must both be host or both device");
+        }
+        cuda(cudaMalloc(&d_pk, n * 8), "device hash pre-images");
+    };
+    feed.keys_for_seed = [&](uint64_t seed, int sms) -> const uint64_t* {
+        phg::DevIndex ix{};
+        ix.seed = seed;
+        ix.hash_algo = hash_algo;
+        {  // AES round keys of hash.cpp:116-119
+            auto mix64 = [](uint64_t z) {
+                z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+                z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+                return z ^ (z >> 31);
+            };
+            const uint64_t w0[2] = {seed + kGolden, seed ^ 0x8bb84b93962eacc9ULL};
+            const uint64_t w1[2] = {(~seed) * 0x6c62272e07bb0143ULL, mix64(seed) ^ 0x2d358dccaa6c78a5ULL};
+            for (int i = 0; i < 4; i++) {
+                ix.aes_k0[i] = (uint32_t)(w0[i / 2] >> (32 * (i % 2)));
+                ix.aes_k1[i] = (uint32_t)(w1[i / 2] >> (32 * (i % 2)));
+            }
+        }
+        const cudaError_t e = phg::launch_hash_bytes(ix, db, dof, d_pk, n, cinv, nullptr, sms);
+        if (e != cudaSuccess) throw BuildFail(PH_E_CUDA, std::string("string hash kernel: ") + cudaGetErrorString(e));
+        return d_pk;
+    };
+    const int rc = build_impl(n, params, threads, device, feed, ptrh, len, stats);
+    if (d_bytes) cudaFree(d_bytes);
+    if (d_offs) cudaFree(d_offs);
+    if (d_pk) cudaFree(d_pk);
     return rc;
 }
 

@@ -96,6 +96,11 @@ cudaError_t build_prepare_u64(const uint64_t* keys, uint64_t n, uint64_t P, uint
                               uint64_t seed, uint64_t* hashes, uint64_t* offsets, int* status,
                               cudaStream_t s, int sms);
 
+// ph_query_bytes.cu: the string hash of every key as u64 pre-images of the integer hash
+// (string-key construction). ix: seed, hash_algo and AES round keys only.
+cudaError_t launch_hash_bytes(const DevIndex& ix, const uint8_t* bytes, const uint64_t* offsets,
+                              uint64_t* out, uint64_t n, uint64_t cinv, cudaStream_t s, int sms);
+
 // ph_search.cu: the per-part pilot search on the GPU (one CTA per part, 256 pilots at once).
 size_t search_smem_bytes(uint64_t S);
 bool search_parts_supported(uint64_t S, uint64_t B, uint64_t max_part);

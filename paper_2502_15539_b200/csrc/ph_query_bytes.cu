@@ -554,6 +554,58 @@ __global__ void __launch_bounds__(kBytesThreads, 1) k_query_bytes(const DevIndex
     }
 }
 
+// Construction of a string-key index (ph_builder.cu): hash_bytes(key, seed).lo of every key
+// (hash.cpp:159-193; what build(span<const std::string>) feeds run_attempt<H64>,
+// construction.cpp:159-171), written as its pre-image under the integer hash,
+// out[i] = Cinv * lo ^ seed, so that the u64 build front (C * (out[i] ^ seed) == lo) sorts
+// and searches exactly the string hashes. One key per thread; the AES tables as in
+// k_query_bytes. Only ix.seed, ix.hash_algo and the AES round keys of ix are used.
+__global__ void __launch_bounds__(kBytesThreads, 1) k_hash_bytes(const DevIndex ix,
+                                                                  const uint8_t* __restrict__ data,
+                                                                  const uint64_t* __restrict__ offsets,
+                                                                  uint64_t* __restrict__ out,
+                                                                  uint64_t nkeys, uint64_t cinv) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const uint32_t win = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    if (win + sizeof(BytesLow) > kTabBase) __trap();
+    BytesLow& SM = *reinterpret_cast<BytesLow*>(smem_raw);
+    AesTables& T = *reinterpret_cast<AesTables*>(smem_raw + (kTabBase - win));
+    const unsigned lane = threadIdx.x & 31;
+    const SmemLook tb{kTabBase + lane * 4};
+    const uint32_t init_s = (uint32_t)__cvta_generic_to_shared(SM.init);
+    if (ix.hash_algo == 1 || ix.hash_algo == 2) {
+        fill_tables(T);
+        __syncthreads();
+        const uint32_t k0[4] = {ix.aes_k0[0], ix.aes_k0[1], ix.aes_k0[2], ix.aes_k0[3]};
+        for (uint32_t len = threadIdx.x; len < kInitLens; len += blockDim.x) {
+            uint32_t st[4];
+            set128(st, (uint64_t)len * kC, ix.seed ^ (uint64_t)len);  // hash.cpp:120-122
+            aesenc(st, k0, tb);
+            SM.init[len] = make_uint4(st[0], st[1], st[2], st[3]);
+        }
+        __syncthreads();
+    }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nkeys;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t hi, lo;
+        hash_key<false, true>(data, __ldg(offsets + i), __ldg(offsets + i + 1), ix, init_s, tb, hi, lo);
+        out[i] = (cinv * lo) ^ ix.seed;
+    }
+}
+
+cudaError_t launch_hash_bytes(const DevIndex& ix, const uint8_t* bytes, const uint64_t* offsets,
+                              uint64_t* out, uint64_t n, uint64_t cinv, cudaStream_t s, int sms) {
+    if (n == 0) return cudaSuccess;
+    constexpr size_t smem = kBytesSmem;
+    cudaError_t e = cudaFuncSetAttribute(k_hash_bytes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t want = (n + kBytesThreads - 1) / kBytesThreads;
+    const int blocks = (int)(want < (uint64_t)sms ? want : (uint64_t)sms);
+    k_hash_bytes<<<blocks, kBytesThreads, smem, s>>>(ix, bytes, offsets, out, n, cinv);
+    note_launch();
+    return cudaGetLastError();
+}
+
 template <int G, bool POW2, class OutT>
 static cudaError_t launch_b(const DevIndex& ix, const uint8_t* d, const uint64_t* o,
                             uint64_t bo, void* out, uint64_t n, int minimal, cudaStream_t s, int sms) {

@@ -259,6 +259,32 @@ def build_u64(keys, params: BuildParams | None = None, threads: int = 0, device:
     return (b, st.as_dict()) if stats else b
 
 
+_L.ph_gpu_build_bytes.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(BuildParams), C.c_int,
+                                  C.c_uint, C.c_int, C.POINTER(u8p), C.POINTER(C.c_size_t),
+                                  C.POINTER(BuildStats)]
+
+
+def build_bytes(data, offsets, params: BuildParams | None = None, hash_algo: int = 1, threads: int = 0,
+                device: int = 0, stats: bool = False):
+    """build(span<const std::string>) + serialize() (construction.cpp:154-226) for keys given as
+    concatenated bytes `data` (numpy u8 or CUDA uint8 tensor) + u64 `offsets[n+1]`: PTRH v1
+    bytes of a string-key index hashed with aes64 (1) or portable64 (3)."""
+    params = params if params is not None else build_params()
+    if _is_torch(data):
+        n = offsets.numel() - 1
+        dp, op = data.data_ptr(), offsets.data_ptr()
+    else:
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        n = offsets.size - 1
+        dp, op = (data.ctypes.data if data.size else None), offsets.ctypes.data
+    out, ln, st = u8p(), C.c_size_t(0), BuildStats()
+    _check(_L.ph_gpu_build_bytes(C.c_void_p(dp), C.c_void_p(op), n, C.byref(params), hash_algo, threads,
+                                 device, C.byref(out), C.byref(ln), C.byref(st)))
+    b = _take_ptrh(out, ln)
+    return (b, st.as_dict()) if stats else b
+
+
 def build_from_sorted_u64(hashes: np.ndarray, offsets: np.ndarray, params: BuildParams, seed: int,
                           threads: int = 0, stats: bool = False):
     """The host stage of one build attempt (no GPU): sorted part-major hashes + part offsets

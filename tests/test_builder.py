@@ -336,3 +336,60 @@ def test_gpu_search_falls_back_for_large_parts(ref):
         assert got1 == want1 and st1["search_on_gpu"]
     finally:
         ph.set_build_search(0)
+
+# ---- GPU: string-key builds ----
+
+def _concat(strs):
+    offs = np.zeros(len(strs) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(s) for s in strs])
+    data = np.frombuffer(b"".join(strs) or b"\0", dtype=np.uint8).copy()
+    return data, offs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset,kw", [("default", dict(lambda_=(30, 10))), ("fast", {}),
+                                       ("compact", dict(remap="elias-fano"))])
+def test_gpu_build_bytes_matches_reference(ref, preset, kw, search_mode):
+    """build(span<const std::string>) + serialize(): the string hash (aes64, what the reference
+    picks on this host) runs on the GPU and the 64-bit hashes go through the u64 front and the
+    pilot search; the bytes equal the reference's, from host and from device buffers, with the
+    edge lengths (empty, 1, 15, 16, 17, 200, 1024 bytes) among the keys."""
+    torch = _cuda()
+    ph = _ph()
+    from oracle.bindings import string_corpus
+    strs = string_corpus(120_000, 31) + [b"", b"a", b"q" * 15, b"x" * 16, b"y" * 17, b"z" * 200,
+                                         bytes(range(256)) * 4]
+    data, offs = _concat(strs)
+    want = ref.build_bytes(data, offs, ref.params(preset, **kw))
+    assert want[8] == 1 and want[9] == 1, "the reference picked another string hash on this host"
+    got, st = ph.build_bytes(data, offs, ph.build_params(preset, **kw), hash_algo=1, stats=True)
+    assert got == want
+    assert st["n"] == len(strs) and st["search_on_gpu"] == (search_mode == 2)
+    d = torch.from_numpy(data).cuda()
+    o = torch.from_numpy(offs.view(np.int64)).cuda()
+    assert ph.build_bytes(d, o, ph.build_params(preset, **kw), hash_algo=1) == want
+
+
+@pytest.mark.gpu
+def test_gpu_build_bytes_portable64_and_errors(ref):
+    """portable64 (the reference's choice on hosts without AES-NI): the built index is a
+    bijection on its keys when queried through the GPU path, and identical keys (equal
+    fingerprints under every seed) end like the reference's persistent-duplicate failure."""
+    _cuda()
+    ph = _ph()
+    from oracle.bindings import string_corpus
+    strs = string_corpus(60_000, 32)
+    data, offs = _concat(strs)
+    b = ph.build_bytes(data, offs, ph.build_params("default", lambda_=(30, 10)), hash_algo=3)
+    assert b[8] == 1 and b[9] == 3
+    idx = ph.PtrHashIndex(b)
+    got = idx.query((data, offs), out_width=4).astype(np.uint64)
+    assert np.array_equal(np.sort(got), np.arange(len(strs), dtype=np.uint64))
+    dup = strs[:1000] + [strs[7]]
+    d2, o2 = _concat(dup)
+    with pytest.raises(ph.PhGpuError) as e:
+        ph.build_bytes(d2, o2, ph.build_params("default"), hash_algo=1)
+    assert e.value.code == ph.E_UNSUPPORTED
+    with pytest.raises(ph.PhGpuError) as e:
+        ph.build_bytes(data, offs, ph.build_params("default"), hash_algo=2)
+    assert e.value.code == ph.E_UNSUPPORTED

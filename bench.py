@@ -391,7 +391,34 @@ class StrWork:
             ref = Ref()
             log(f"[fixture] {n} strings ({hd.size / 1e9:.1f} GB) generated; reference "
                 f"build_sharded over the concatenated buffer...")
-            return ref.build_bytes(hd, ho, ref_params(ref), lean=True)
+            t = time.time()
+            ptrh = ref.build_bytes(hd, ho, ref_params(ref), lean=True)
+            ref_s = time.time() - t
+            if args.construction and dist.world == 1 and ptrh[9] == 1:
+                # Construction (off the query path): the same strings through ph_gpu_build_bytes
+                # (string hash, sort and pilot search on the GPU), wall clock from host buffers
+                gp = ph_gpu.build_params("default", lambda_=(30, 10))
+                ph_gpu.build_bytes(hd[:int(ho[100_000])], ho[:100_001], gp)  # untimed: loads the kernels
+                t = time.time()
+                ours, st = ph_gpu.build_bytes(hd, ho, gp, hash_algo=1, stats=True)
+                ours_s = time.time() - t
+                same = ours == ptrh
+                log(f"[construction] strings: reference {ref_s:.1f}s, ours {ours_s:.1f}s, PTRH identical: {same}")
+                if not same:
+                    raise SystemExit("construction: ph_gpu_build_bytes bytes differ from the reference's")
+                self.construction = {
+                    "what": "build(span<string>) + serialize() of this config's index from host-resident "
+                            "bytes + offsets: the reference (build_sharded, one shard, all host threads) vs "
+                            "ph_gpu_build_bytes (aes64 string hash, MSD radix sort and pilot search on the "
+                            "GPU, remap table on the host); wall clock, one run each, after one untimed "
+                            "1e5-key build that loads the kernels",
+                    "n": int(n), "reference_s": round(ref_s, 3), "ours_s": round(ours_s, 3),
+                    "speedup": round(ref_s / ours_s, 3), "host_threads": int(ref.hw_threads()),
+                    "identical_ptrh": same, "attempts": st["attempts"],
+                    "search_on_gpu": bool(st.get("search_on_gpu")),
+                    "stages_ms": {k: round(st[k], 1) for k in
+                                  ("upload_ms", "prepare_ms", "search_ms", "remap_ms", "total_ms")}}
+            return ptrh
 
         self.ptrh = build_index_bytes(n, dist, None, build=build, tag="str")
         self.idx = ph_gpu.PtrHashIndex(self.ptrh, device=dist.local)

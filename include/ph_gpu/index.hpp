@@ -180,4 +180,23 @@ inline std::vector<uint8_t> build(std::span<const uint64_t> keys, const ph_build
     return out;
 }
 
+// build(std::span<const std::string>, params, threads, stats) + serialize()
+// (construction.cpp:154-226) with the 64-bit string hashes (hash_algo 1 = aes64, the
+// reference's pick on an x86 host with AES-NI; 3 = portable64).
+inline std::vector<uint8_t> build(std::span<const std::string> keys, const ph_build_params& params,
+                                  int hash_algo = 1, unsigned threads = 0, int device = 0,
+                                  ph_build_stats* stats = nullptr) {
+    std::vector<uint64_t> offsets(keys.size() + 1, 0);
+    for (size_t i = 0; i < keys.size(); i++) offsets[i + 1] = offsets[i] + keys[i].size();
+    std::vector<uint8_t> bytes(offsets.back() ? offsets.back() : 1);
+    for (size_t i = 0; i < keys.size(); i++) std::copy(keys[i].begin(), keys[i].end(), bytes.begin() + offsets[i]);
+    uint8_t* out_bytes = nullptr;
+    size_t len = 0;
+    check(ph_gpu_build_bytes(bytes.data(), offsets.data(), keys.size(), &params, hash_algo, threads, device,
+                             &out_bytes, &len, stats));
+    std::vector<uint8_t> out(out_bytes, out_bytes + len);
+    ph_free(out_bytes);
+    return out;
+}
+
 }  // namespace ph_gpu

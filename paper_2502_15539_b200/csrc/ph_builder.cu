@@ -1167,7 +1167,7 @@ int ph_gpu_build_bytes(const uint8_t* bytes, const uint64_t* offsets, size_t n,
     feed.key_kind = 1;
     feed.hash_algo = (uint8_t)hash_algo;
     feed.dup_is_error = false;
-    feed.upload = [&](unsigned, int) {
+    feed.upload = [&](unsigned th, int dev) {
         auto cuda = [](cudaError_t e, const char* what) {
             if (e == cudaErrorMemoryAllocation) throw BuildFail(PH_E_NOMEM, what);
             if (e != cudaSuccess) throw BuildFail(PH_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -1179,10 +1179,21 @@ int ph_gpu_build_bytes(const uint8_t* bytes, const uint64_t* offsets, size_t n,
             if (total && !bytes) throw BuildFail(PH_E_INVALID, "null bytes");
             if (is_device_ptr(bytes)) throw BuildFail(PH_E_INVALID, "bytes and offsets must both be host or both device");
             cuda(cudaMalloc(&d_offs, (n + 1) * 8), "device offsets of the keys");
-            cuda(cudaMemcpy(d_offs, offsets, (n + 1) * 8, cudaMemcpyHostToDevice), "offset upload");
+            cuda(upload_pipelined(d_offs, offsets, n + 1, th, dev), "offset upload");
             cuda(cudaMalloc(&d_bytes, total + 32), "device key bytes");
             // offsets index `bytes`; the device copy starts at offsets[0]
-            cuda(cudaMemcpy(d_bytes, bytes + offsets[0], total, cudaMemcpyHostToDevice), "key byte upload");
+            const uint8_t* hb = bytes + offsets[0];
+            if ((reinterpret_cast<uintptr_t>(hb) & 7) == 0 && total >= 8) {
+                cuda(upload_pipelined(reinterpret_cast<uint64_t*>(d_bytes), reinterpret_cast<const uint64_t*>(hb),
+                                      total / 8, th, dev),
+                     "key byte upload");
+                if (total & 7)
+                    cuda(cudaMemcpy(d_bytes + (total & ~uint64_t{7}), hb + (total & ~uint64_t{7}), total & 7,
+                                    cudaMemcpyHostToDevice),
+                         "key byte upload");
+            } else {
+                cuda(cudaMemcpy(d_bytes, hb, total, cudaMemcpyHostToDevice), "key byte upload");
+            }
             db = d_bytes - offsets[0];
             dof = d_offs;
         } else if (!is_device_ptr(bytes)) {

@@ -209,6 +209,8 @@ int main(int argc, char** argv) {
         if (R.build_bytes(bytes.data(), offs.data(), keys.size(), &p, 0, &b, &blen) != 0) return 3;
         std::vector<uint8_t> ptrh(b, b + blen);
         R.free_(b);
+        // the same index built on the GPU through the C++ wrapper (aes64, the reference's pick here)
+        if (ptrh[9] == 1) CHECK(ph_gpu::build(std::span<const std::string>(keys), ph_gpu::preset("default")) == ptrh);
         void* ref = R.load(ptrh.data(), ptrh.size());
         const ph_gpu::PtrHashIndex idx(ptrh);
         const size_t m = keys.size();

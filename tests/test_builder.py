@@ -393,3 +393,24 @@ def test_gpu_build_bytes_portable64_and_errors(ref):
     with pytest.raises(ph.PhGpuError) as e:
         ph.build_bytes(data, offs, ph.build_params("default"), hash_algo=2)
     assert e.value.code == ph.E_UNSUPPORTED
+
+@pytest.mark.gpu
+def test_gpu_build_tiny_inputs(ref):
+    """1 to 1000 keys (parts with a single bucket, a single key, the empty string as a key):
+    u64 and string builds with the GPU search forced give the reference's bytes."""
+    _cuda()
+    ph = _ph()
+    from oracle.bindings import string_corpus
+    ph.set_build_search(2)
+    try:
+        for n in (1, 2, 3, 7, 33, 257, 1000):
+            keys = corpus_u64_np(0, n, 1000 + n)
+            for preset in ("default", "fast", "compact"):
+                got, st = ph.build_u64(keys, ph.build_params(preset), stats=True)
+                assert got == ref.build_u64(keys, ref.params(preset)) and st["search_on_gpu"], (n, preset)
+            strs = string_corpus(n, n, 0, 40) if n > 1 else [b""]
+            data, offs = _concat(strs)
+            assert ph.build_bytes(data, offs, ph.build_params("default")) == \
+                ref.build_bytes(data, offs, ref.params("default")), ("strings", n)
+    finally:
+        ph.set_build_search(0)

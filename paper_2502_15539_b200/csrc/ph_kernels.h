@@ -103,6 +103,7 @@ cudaError_t launch_hash_bytes(const DevIndex& ix, const uint8_t* bytes, const ui
 
 // ph_search.cu: the per-part pilot search on the GPU (one CTA per part, 256 pilots at once).
 size_t search_smem_bytes(uint64_t S);
+int search_check_errors(uint64_t* count, uint64_t* line);  // checked builds (ph_search.cu)
 bool search_parts_supported(uint64_t S, uint64_t B, uint64_t max_part);
 cudaError_t search_parts_gpu(const uint64_t* d_hashes, const uint64_t* d_off, uint64_t n, uint64_t P,
                              uint64_t S, uint64_t B, uint64_t seed, int fn, const uint64_t* d_opt,

@@ -933,6 +933,11 @@ int check_errors(uint64_t* count, uint64_t* line) {
     cudaMemcpyToSymbol(g_chk, z, sizeof(z));
     *count = h[0];
     *line = h[1];
+    uint64_t sc = 0, sl = 0;  // the pilot-search kernel's counters (ph_search.cu)
+    if (search_check_errors(&sc, &sl) == 0 && sc) {
+        if (!*count) *line = 1000000 + sl;  // (lines of ph_search.cu are reported + 1e6)
+        *count += sc;
+    }
     return 0;
 #else
     *count = *line = 0;

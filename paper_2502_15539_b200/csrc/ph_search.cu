@@ -52,8 +52,24 @@ constexpr uint32_t kHeapCap = 512;      // pending evicted buckets (shared-memor
 constexpr uint32_t kNoBucket = 0xffffffffu;  // engine.hpp:91
 constexpr int kRecent = 16;             // engine.hpp:92
 
+// Checked builds (-DPH_CHECKS, tools/checked_run.py): slots, visiting indices, bucket ids,
+// hash positions and heap sizes are bounds-checked on the device; violations are counted and
+// read back with ph_gpu_check_errors (compute-sanitizer cannot attach on this GPU pool).
+#ifdef PH_CHECKS
+__device__ unsigned long long g_schk[2];  // [0] violations, [1] source line of the first
+#define PH_SCHECK(c)                                                                   \
+    do {                                                                               \
+        if (!(c) && atomicAdd(&g_schk[0], 1ull) == 0) g_schk[1] = __LINE__;           \
+    } while (0)
+#else
+#define PH_SCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 struct Arith {
     uint64_t P, S, B, seed, fm;  // fm = floor((2^64 - 1) / S)
+    uint64_t hre_cap;            // entries of a workspace's hre[] (checked builds)
     const uint64_t* opt;
     int fn, p2;
     ModFast mf;                  // 32-bit form of y mod S for 2^13 <= S < 2^21 (ph_arith.cuh)
@@ -119,6 +135,7 @@ __device__ __forceinline__ unsigned long long bkey(uint32_t b, uint32_t sz) {
     return ((unsigned long long)sz << 32) | (0xffffffffu - b);  // engine.hpp:335 heap order
 }
 __device__ void heap_push(Shared& sm, unsigned long long k) {
+    PH_SCHECK(sm.hn < kHeapCap);
     uint32_t i = sm.hn++;
     while (i) {
         const uint32_t p = (i - 1) >> 1;
@@ -129,6 +146,7 @@ __device__ void heap_push(Shared& sm, unsigned long long k) {
     sm.heap[i] = k;
 }
 __device__ void heap_pop(Shared& sm) {
+    PH_SCHECK(sm.hn >= 1 && sm.hn <= kHeapCap);
     const unsigned long long k = sm.heap[--sm.hn];
     uint32_t i = 0;
     for (;;) {
@@ -163,6 +181,7 @@ __device__ __forceinline__ bool test_pilot_reg(const Arith& a, const uint32_t* t
         r[i] = 0xffffffffu - i;  // beyond kc: distinct dummies (slots are < 2^31)
         if (i < (int)kc) {
             r[i] = slot_of_y(a, kq[i] ^ hl);
+            PH_SCHECK(r[i] < a.S);
             busy |= taken[r[i] >> 5] >> (r[i] & 31);
         }
     }
@@ -278,6 +297,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
             const unsigned long long ki = __ldcg(w.bigk + i);
             uint32_t rank = 0;
             for (uint32_t j = 0; j < nbig; j++) rank += __ldcg(w.bigk + j) > ki;
+            PH_SCHECK(rank < nbig);
             w.ord[rank] = 0xffffffffu - (uint32_t)ki;
         }
         if (tid == 0) {  // class tables: sizes descending, within a size warps ascending
@@ -314,6 +334,8 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
             if (sz && rank == 0) sm.wbase[warp][sz] += __popc(mm);
             __syncwarp();
             if (sz) {
+                PH_SCHECK(idx < nonempty && idx >= sm.cbeg[sz] && idx < sm.cbeg[sz] + sm.cnt[sz] &&
+                          sm.cpos[sz] + (uint64_t)(idx - sm.cbeg[sz] + 1) * sz <= a.hre_cap);
                 w.ord[idx] = b;
                 uint64_t* dst = w.hre + sm.cpos[sz] + (uint64_t)(idx - sm.cbeg[sz]) * sz;
                 for (uint32_t i = 0; i < sz; i++) dst[i] = h[st + i];
@@ -354,7 +376,10 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                 if (q < nb) {
                     if (c >= cend)
                         while (c >= sm.cbeg[kc] + sm.cnt[kc]) kc--;
+                    PH_SCHECK(c < nonempty && kc >= 1 && kc <= kMaxK && c >= sm.cbeg[kc] &&
+                              sm.cpos[kc] + (uint64_t)(c - sm.cbeg[kc] + 1) * kc <= a.hre_cap);
                     mybk = w.ord[c];
+                    PH_SCHECK(mybk < B);
                     const uint64_t* kq = w.hre + sm.cpos[kc] + (uint64_t)(c - sm.cbeg[kc]) * kc;
                     uint32_t win = 32, round = 0;
                     uint32_t r8[kRegK];
@@ -424,6 +449,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                 uint32_t s2 = 0;
                 if (q < nf && warp == mybw && lane < kc) {
                     s2 = sm.bsl[warp][lane];
+                    PH_SCHECK(s2 < S && mybw < kSThreads / 32);
                     hit = (atomicOr(&taken[s2 >> 5], 1u << (s2 & 31)) >> (s2 & 31)) & 1;
                     claimed = !hit;
                 }
@@ -492,6 +518,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
             if (hn && (cursor == nonempty || sm.heap[0] > bkey(bk, k))) from_heap = true;
             if (from_heap) {
                 bk = 0xffffffffu - (uint32_t)sm.heap[0];
+                PH_SCHECK(bk < B);
                 const uint32_t st = __ldcg(w.start + bk);
                 k = __ldcg(w.start + bk + 1) - st;
                 kh = h + st;
@@ -651,6 +678,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
             if (pstar < 256) {
                 if (tid == pstar) {
                     for (uint32_t i = 0; i < k; i++) {
+                        PH_SCHECK(sl[i] < S && bk < B);
                         taken[sl[i] >> 5] |= 1u << (sl[i] & 31);
                         w.owner[sl[i]] = bk;
                     }
@@ -702,8 +730,10 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
                         if (v != kNoBucket) {  // displace v entirely
                             const uint64_t vhp = kC * ((uint64_t)__ldcg(pl + v) ^ a.seed);
                             const uint32_t v0 = __ldcg(w.start + v), v1 = __ldcg(w.start + v + 1);
+                            PH_SCHECK(v < B && v0 <= v1 && v1 <= m);
                             for (uint32_t j = v0; j < v1; j++) {
                                 const uint32_t vs = slot_of_y(a, h[j] ^ vhp);
+                                PH_SCHECK(vs < S && ((taken[vs >> 5] >> (vs & 31)) & 1));  // v held it
                                 taken[vs >> 5] &= ~(1u << (vs & 31));
                                 __stcg(w.owner + vs, kNoBucket);
                             }
@@ -763,6 +793,22 @@ __global__ void __launch_bounds__(kSThreads, 2) k_search_parts(
 
 }  // namespace
 
+// Violations counted by a checked build's search kernel since the last call; -1 otherwise.
+int search_check_errors(uint64_t* count, uint64_t* line) {
+#ifdef PH_CHECKS
+    unsigned long long h[2] = {0, 0};
+    if (cudaMemcpyFromSymbol(h, g_schk, sizeof(h)) != cudaSuccess) return -2;
+    const unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_schk, z, sizeof(z));
+    *count = h[0];
+    *line = h[1];
+    return 0;
+#else
+    *count = *line = 0;
+    return -1;
+#endif
+}
+
 size_t search_smem_bytes(uint64_t S) {
     return ((sizeof(Shared) + 15) & ~size_t{15}) + ((S + 31) / 32) * 4;
 }
@@ -790,6 +836,7 @@ cudaError_t search_parts_gpu(const uint64_t* d_hashes, const uint64_t* d_off, ui
     a.fn = fn;
     a.mf = mod_fast_make(S);
     if (a.p2) a.mf.ok = false;
+    a.hre_cap = max_part + 128;
     const uint32_t words = (uint32_t)((S + 31) / 32);
     const size_t smem = search_smem_bytes(S);
     cudaError_t e = cudaFuncSetAttribute(k_search_parts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -10,7 +10,8 @@ passes A-C, plus a canary band after the scratch), and for each case:
     difference between launch shapes or repeats.
 Cases: u64 batches of 1, 4095..4097, 1e6+3 keys; unaligned key / output pointers; a single
 key repeated (the spill region); keys sorted by group; many groups (small slices); k-mer
-sources at the tile-edge sizes; u32 and u64 outputs; minimal and non-minimal.
+sources at the tile-edge sizes; u32 and u64 outputs; minimal and non-minimal; and builds
+(u64 and string keys) with the GPU pilot search, whose kernel carries its own assertions.
 
   python tools/checked_run.py   (PH_GPU_LIB defaults to variants/libph_gpu_checked.so)
 """
@@ -130,6 +131,44 @@ def main():
         for kk in ("PH_GPU_PART_A_CTAS", "PH_GPU_PART_B_CTAS", "PH_GPU_PART_C_CTAS"):
             os.environ.pop(kk, None)
         kidx.close()
+    # construction: builds with the GPU pilot search forced, on the checked library (slots,
+    # visiting indices, bucket ids, hash positions and heap sizes asserted on the device);
+    # repeated builds must give the same bytes, equal to the reference's
+    ph_gpu.set_partition(0)
+    ph_gpu.set_build_search(2)
+    from oracle.bindings import string_corpus
+    build_cases = [("default l=3.0 n=300k", "default", dict(lambda_=(30, 10)), 300_000),
+                   ("compact (evictions) n=300k", "compact", {}, 300_000),
+                   ("fast pow2 n=150k", "fast", dict(reduce="pow2-mul"), 150_000),
+                   ("optimal gamma, forced shape n=40k", "default",
+                    dict(bucket_fn="optimal", shape=(3, 20_000, 3_000)), 40_000),
+                   ("tiny n=7", "default", {}, 7)]
+    for name, preset, kw, bn in build_cases:
+        bk = corpus_u64_np(0, bn, 900 + bn)
+        if "shape" in kw:
+            want = ref.build_u64_shape(bk, ref.params(preset, **{k: v for k, v in kw.items() if k != "shape"}),
+                                       *kw["shape"])
+        else:
+            want = ref.build_u64(bk, ref.params(preset, **kw))
+        outs = [ph_gpu.build_u64(bk, ph_gpu.build_params(preset, **kw)) for _ in range(2)]
+        errs = check_errors()
+        results.append({"case": f"build u64: {name}", "minimal": None, "width": None, "keys": bn,
+                        "bit_exact": bool(outs[0] == want),
+                        "identical_across_shapes_and_repeats": bool(outs[0] == outs[1]),
+                        "check_violations": errs[0], "first_line": errs[1]})
+        print(json.dumps(results[-1]), flush=True)
+    strs = string_corpus(80_000, 5) + [b"", b"x" * 300]
+    so = np.zeros(len(strs) + 1, dtype=np.uint64)
+    so[1:] = np.cumsum([len(x) for x in strs])
+    sd = np.frombuffer(b"".join(strs), dtype=np.uint8).copy()
+    want = ref.build_bytes(sd, so, ref.params("default"))
+    outs = [ph_gpu.build_bytes(sd, so, ph_gpu.build_params("default")) for _ in range(2)]
+    errs = check_errors()
+    results.append({"case": "build strings (aes64) n=80k", "minimal": None, "width": None, "keys": len(strs),
+                    "bit_exact": bool(outs[0] == want), "identical_across_shapes_and_repeats": bool(outs[0] == outs[1]),
+                    "check_violations": errs[0], "first_line": errs[1]})
+    print(json.dumps(results[-1]), flush=True)
+    ph_gpu.set_build_search(0)
     ok = all(r["bit_exact"] and r["identical_across_shapes_and_repeats"] and r["check_violations"] == 0
              for r in results)
     print(f"CHECKED RUN {'CLEAN' if ok else 'FAILED'}: {len(results)} cases", flush=True)

@@ -631,7 +631,7 @@ def run_ours(args, cfg):
         p_in = torch.empty(nl, dtype=torch.int64, device="cuda")
         p_out = torch.empty(nl, dtype=torch.int32, device="cuda")
         run_port = lambda: bench.phb_port_model(  # noqa: E731
-            C.c_void_p(pil.data_ptr()), C.c_uint64(slice_bytes), C.c_uint64(nl), C.c_uint64(1), 1, 4,
+            C.c_void_p(pil.data_ptr()), C.c_uint64(slice_bytes), C.c_uint64(nl), C.c_uint64(1), 1, 42,
             C.c_void_p(p_in.data_ptr()), C.c_void_p(p_out.data_ptr()), C.c_void_p(sink.data_ptr()), sp)
         port_ms = time_ms(run_port, 3)
         r_port = nl / port_ms / 1e6
@@ -762,7 +762,8 @@ def run_ours(args, cfg):
                       "peak_gsectors_s": round(r_port or r_gather_slice, 2),
                       "peak_source": (f"live k_port microbenchmark: random 1-byte gathers over "
                                       f"{slice_bytes >> 20} MiB with 8 B streamed in and 4 B out "
-                                      f"per gather (tools/port_model.py, DESIGN.md §3)"
+                                      f"per gather, two outputs per store like the pass "
+                                      f"(tools/port_model.py, DESIGN.md §3)"
                                       if r_port else
                                       f"live k_gather microbenchmark over {slice_bytes >> 20} MiB"),
                       "frac": round(gathers_b / (r_port or r_gather_slice), 4),

@@ -181,6 +181,16 @@ __global__ void __launch_bounds__(256, 4) k_port(const uint8_t* __restrict__ buf
             if (OUT == 4)
                 asm volatile("st.global.cs.u32 [%0], %1;" ::"l"((uint32_t*)sout + base + j * 32 + lane),
                              "r"(v[j] + (uint32_t)kv[j]) : "memory");
+            else if (OUT == 42) {  // 4 B per gather, two per store (pass B's st.global.cs.v2.u32)
+                if (j & 1)
+                    asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"((uint32_t*)sout + base + (j >> 1) * 64 + lane * 2),
+                                 "r"(v[j - 1] + (uint32_t)kv[j - 1]), "r"(v[j] + (uint32_t)kv[j]) : "memory");
+            } else if (OUT == 44) {  // 4 B per gather, four per store
+                if ((j & 3) == 3)
+                    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"((uint32_t*)sout + base + (j >> 2) * 128 + lane * 4),
+                                 "r"(v[j - 3] + (uint32_t)kv[j - 3]), "r"(v[j - 2] + (uint32_t)kv[j - 2]),
+                                 "r"(v[j - 1] + (uint32_t)kv[j - 1]), "r"(v[j] + (uint32_t)kv[j]) : "memory");
+            }
             else if (OUT == 8)
                 asm volatile("st.global.cs.u64 [%0], %1;" ::"l"((uint64_t*)sout + base + j * 32 + lane),
                              "l"(kv[j] + v[j]) : "memory");
@@ -536,6 +546,7 @@ int phb_port_model(const uint8_t* d_buf, uint64_t F, uint64_t nloads, uint64_t s
         k_port_bulk<<<sms * 4, 256, 0, s>>>(d_buf, F, nloads, seed, d_sin, (uint32_t*)d_sout, d_sink);
         return (int)cudaGetLastError();
     }
+    PH_PORT(1, 42) PH_PORT(1, 44)
     PH_PORT(0, 0) PH_PORT(1, 0) PH_PORT(2, 0) PH_PORT(0, 4) PH_PORT(1, 4) PH_PORT(1, 8) PH_PORT(2, 4) PH_PORT(2, 8)
 #undef PH_PORT
     return (int)cudaErrorInvalidValue;

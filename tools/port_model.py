@@ -42,7 +42,7 @@ def main():
     st = torch.cuda.current_stream().cuda_stream
     rows = []
     base = None
-    for in_w, out_b in ((0, 0), (1, 0), (2, 0), (0, 4), (1, 4), (1, -4), (1, 8), (2, 4), (2, 8)):  # -4: bulk stores
+    for in_w, out_b in ((0, 0), (1, 0), (2, 0), (0, 4), (1, 4), (1, 42), (1, 44), (1, -4), (1, 8), (2, 4), (2, 8)):  # -4: bulk stores
         def run():
             assert lib.phb_port_model(buf.data_ptr(), F, n, 7, in_w, out_b, sin.data_ptr(),
                                       sout.data_ptr(), sink.data_ptr(), st) == 0
@@ -62,8 +62,10 @@ def main():
         ms = min(ts)
         if base is None:
             base = ms
-        sect = 1 + in_w * 8 / 32 + abs(out_b) / 32
-        row = {"buffer_mb": a.mb, "gathers": n, "in_bytes": in_w * 8, "out_bytes": abs(out_b), "out_path": "smem + cp.async.bulk" if out_b < 0 else "st.global.cs",
+        ob = 4 if out_b in (42, 44) else abs(out_b)
+        sect = 1 + in_w * 8 / 32 + ob / 32
+        row = {"buffer_mb": a.mb, "gathers": n, "in_bytes": in_w * 8, "out_bytes": ob, "out_path": ("smem + cp.async.bulk" if out_b < 0 else "st.global.cs.v2.u32" if out_b == 42
+                                                 else "st.global.cs.v4.u32" if out_b == 44 else "st.global.cs"),
                "ms": round(ms, 4), "ggathers_s": round(n / ms / 1e6, 2),
                "port_sectors_per_gather": round(sect, 4),
                "gsectors_s": round(n * sect / ms / 1e6, 2),
